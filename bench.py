@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""CB-SpMV benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat|clustered|laplace|uniform]
+                    [--dtype f64|f32] [--impl cb|reference]
+
+A step is one y := A·x over the whole (row-sharded) matrix through the C ABI
+(cbspmv_spmv: zero y + the persistent SpMV kernel).  Inputs already resident in
+HBM; the matrix stream (>= 2 GB on the default workload) is far larger than the
+126 MB L2, so back-to-back steps read it from HBM; a cold-L2 figure (L2 flushed
+between individually timed steps) is reported beside it.  Multi-GPU: one
+process per GPU under torchrun, rows split by nnz at block-row boundaries (no
+data-path collective for a single SpMV), time = max over ranks.
+
+--impl reference times the oracle (plain single-threaded C, the CPU baseline of
+this tier) on rank 0 on a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 SpMV GFLOP/s and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
+WORKLOAD = {
+    "rmat": "BASELINE configs[2]: synthetic R-MAT scale 23, edge factor 16 (8,388,608 rows, ~131M nnz after dedup)",
+    "clustered": "BASELINE configs[3]: synthetic block-clustered 2^22 rows, ~407M nnz, dense/CSR/COO mix",
+    "laplace": "BASELINE configs[1]: 5-point Laplacian on a 1000x1000 grid (1M rows, 4,996,000 nnz)",
+    "uniform": "BASELINE configs[4] (row shard sizes): uniform random 2^25 rows x 50/row",
+}
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+# ----------------------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    """Sample SM clock + throttle reasons with NVML every ~5 ms during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+            time.sleep(0.02)
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+def make_matrix(config: str, rank: int, world: int):
+    """Generate this rank's row shard (rows split by nnz at block-row boundaries)."""
+    import synth
+    from paper_2605_18515_b200 import dist
+    A = synth.make(config)
+    if world == 1:
+        return A, (0, A.m), A.nnz
+    cuts = dist.equal_bounds(A.m, world) if config == "uniform" else dist.shard_bounds(A.row_ptr, world)
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    return dist.slice_rows(A, r0, r1), (r0, r1), A.nnz
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic(config: str, dtype: str):
+    """dram bytes per launch of the SpMV kernel from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"{config}_{dtype}")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    A = synth.make(args.config)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=7)
+    # bounded sample: leading block-aligned row range sized so the whole run ends in minutes
+    t0 = time.perf_counter()
+    probe_rows = min(A.m, max(16, (A.m // 64) // 16 * 16))
+    from paper_2605_18515_b200.dist import slice_rows
+    oracle.spmv_csr(slice_rows(A, 0, probe_rows), x)
+    t_probe = max(time.perf_counter() - t0, 1e-6)
+    budget = 150.0 / max(1, args.steps + args.warmup)  # seconds per step
+    rows = int(min(A.m, probe_rows * budget / t_probe)) // 16 * 16
+    rows = max(16, min(A.m, rows))
+    S = slice_rows(A, 0, rows)
+    nnz_s = int(S.row_ptr[-1])
+    for _ in range(args.warmup):
+        oracle.spmv_csr(S, x)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.spmv_csr(S, x)
+    dt = (time.perf_counter() - t0) / max(1, args.steps)
+    gflops = 2.0 * nnz_s / dt / 1e9
+    sample = f"rows [0,{rows}) of {A.m} ({nnz_s} of {A.nnz} nnz), full oracle Alg. 1 per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "name": args.config, "m": A.m, "nnz": A.nnz},
+        "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_cb(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2605_18515_b200 as cb
+    from paper_2605_18515_b200 import dist
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+
+    def allreduce(a, op="sum"):
+        if world == 1:
+            return a
+        t = torch.from_numpy(np.asarray(a)).to(dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.SUM if op == "sum" else tdist.ReduceOp.MAX)
+        return t.cpu().numpy()
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    t0 = time.perf_counter()
+    A, (r0, r1), nnz_total = make_matrix(args.config, rank, world)
+    gen_s = time.perf_counter() - t0
+    agg = dist.global_agg(A, lambda a: allreduce(a), dtype=args.dtype) if world > 1 else -1
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0)
+    info = h.info
+    x_host = synth.vector(A.n, synth.VEC_UNIFORM, seed=7)
+    x = torch.from_numpy(x_host).to(dev, tdt)
+    y = torch.empty(A.m, dtype=tdt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # warm-up
+    for _ in range(max(args.warmup, 0)):
+        cb.spmv(h, x, y)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K back-to-back steps (inputs > L2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            cb.spmv(h, x, y)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / max(1, args.steps)
+    ms_max = float(allreduce(np.array([ms]), "max")[0])
+
+    # ---- dominant kernel alone (y += A x, same stream, events over K launches)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    k0.record(stream)
+    for _ in range(args.steps):
+        cb.spmv_add(h, x, y)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kernel_ms = k0.elapsed_time(k1) / max(1, args.steps)
+
+    # ---- cold L2: flush (write 2x L2) before each individually timed step
+    flush = torch.empty(64 << 20, dtype=torch.float64, device=dev)  # 512 MB
+    cold = []
+    for _ in range(min(args.steps, 20)):
+        flush.fill_(1.0)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        cb.spmv(h, x, y)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cold.append(c0.elapsed_time(c1))
+    del flush
+    cold_ms = statistics.median(cold) if cold else None
+
+    # ---- end to end through the public API with host buffers (pinned)
+    vt = np.float64 if args.dtype == "f64" else np.float32
+    xh = torch.from_numpy(x_host.astype(vt)).pin_memory().numpy()
+    yh = torch.empty(A.m, dtype=tdt).pin_memory().numpy()
+    cb.spmv_host(h, xh, yh)
+    barrier()
+    t_e2e = time.perf_counter()
+    for _ in range(args.steps):
+        cb.spmv_host(h, xh, yh)
+    e2e_s = (time.perf_counter() - t_e2e) / max(1, args.steps)
+    e2e_max = float(allreduce(np.array([e2e_s]), "max")[0])
+
+    flops = 2.0 * nnz_total
+    value = flops / (ms_max * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    achieved = info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.config, args.dtype)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(A, x_host, args.dtype)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded generators, synth/)",
+            "config": {
+                "workload": WORKLOAD[args.config], "name": args.config, "m": int(info["m"]) if world == 1 else None,
+                "nnz": int(nnz_total), "agg": int(info["agg"]), "blocks": int(info["nb"]),
+                "fmt_count_coo_csr_dense": list(info["fmt_count"]), "parallelism": f"row-shard x{world}",
+                "l2": "inputs larger than L2 (matrix stream %.2f GB vs 126 MB L2); cold_l2_ms flushes 512 MB "
+                      "before each step" % (info["dev_stream_bytes"] / 1e9),
+                "cold_l2_ms": cold_ms, "cold_l2_gflops": flops / (cold_ms * 1e-3) / 1e9 / world if cold_ms else None,
+                "alg_bytes_per_spmv": int(info["alg_bytes"]), "dev_stream_bytes": int(info["dev_stream_bytes"]),
+                "achieved_hbm_gbs_step": info["alg_bytes"] / (ms * 1e-3) / 1e9,
+                "tb_load_sd": info["tb_load_sd"], "tb_load_sd_natural": info["tb_load_sd_natural"],
+                "gen_s": gen_s, "build_s": info["build_seconds"], "upload_s": info["upload_seconds"],
+                "grid": info["grid"],
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "cb_spmv_kernel",
+                         "kernel_ms": kernel_ms, "peak_source": peak_src,
+                         "bytes": "alg_bytes = 21 B/block meta + |mtx_data| + 4 B/restore entry + "
+                                  "8 B/cols_offset + size(Val)*(n+m), per launch"},
+            "e2e": {"value": flops / e2e_max / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(A.n) * xh.itemsize, "d2h_bytes_per_step": int(A.m) * yh.itemsize,
+                    "path": "cbspmv_spmv_host (pinned host x in, y out, per step)"},
+            "gpu_launches": int(args.steps * info["launches_per_spmv"]),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    cb.destroy(h)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def cpu_baseline(A, x, dtype):
+    """The oracle as it stands (single-threaded C, Alg. 1) on a bounded sample: ~10 s of CPU work."""
+    import oracle
+    import synth
+    from paper_2605_18515_b200.dist import slice_rows
+    if dtype == "f32":
+        A = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
+        x = x.astype(np.float32).astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.spmv_csr(A, x)
+    t1 = time.perf_counter() - t0
+    if t1 > 10.0:  # one full pass is already past the budget: time a leading row sample instead
+        rows = max(16, int(A.m * 10.0 / t1) // 16 * 16)
+        S = slice_rows(A, 0, rows)
+        t0 = time.perf_counter()
+        oracle.spmv_csr(S, x)
+        dt = time.perf_counter() - t0
+        nnz = int(S.row_ptr[-1])
+        return {"value": 2.0 * nnz / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+                "sample": f"rows [0,{rows}) ({nnz} nnz), 1 pass"}
+    reps = int(max(1, min(20, 10.0 / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.spmv_csr(A, x)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": 2.0 * A.nnz / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+            "sample": f"full matrix ({A.nnz} nnz), {reps} passes after 1 warm pass"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="rmat", choices=list(WORKLOAD))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--impl", default="cb", choices=["cb", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_cb(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,192 @@
+/*
+ * cbspmv.h — C ABI of the B200-native CB-SpMV hot path (arxiv 2605.18515).
+ *
+ * y = A·x over the paper's cache-friendly 2D-blocked format ("CB-SpMV",
+ * PAPER.md §3).  Citations "P:<n>" are lines of
+ * /root/reference/PAPER.md; "R-<k>" are the readings of silent or ambiguous
+ * passages listed in DESIGN.md §2.
+ *
+ * Conventions (all entry points):
+ *   - Nothing throws across the ABI; every call returns a cbspmv_status_t and
+ *     stores a human-readable detail retrievable with cbspmv_last_error()
+ *     (thread-local).
+ *   - Indices are 0-based.  A is m x n; x has n entries, y has m entries.
+ *   - "_dev" pointers are CUDA device pointers on the handle's device;
+ *     "_host" pointers are host memory (pinned is fastest, pageable works).
+ *   - stream is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Device calls are asynchronous on that stream; asynchronous
+ *     kernel faults surface at the caller's next synchronisation.
+ *   - The handle owns every device and host allocation it makes; the caller
+ *     owns all buffers it passes in.  Handles are not thread-safe: one thread
+ *     at a time per handle.
+ */
+#ifndef CBSPMV_H
+#define CBSPMV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBSPMV_VERSION 1
+
+typedef struct cbspmv_s *cbspmv_handle_t;
+
+typedef enum {
+  CBSPMV_OK = 0,
+  CBSPMV_EINVAL = 1,      /* bad argument, col >= n, non-finite value, row_ptr decreasing */
+  CBSPMV_EUNSORTED = 2,   /* columns not strictly increasing within a row (R-19) */
+  CBSPMV_ENOMEM = 3,      /* host or device allocation failed */
+  CBSPMV_ECUDA = 4,       /* a CUDA runtime call failed (detail in cbspmv_last_error) */
+  CBSPMV_EDIM = 5,        /* pointer alignment / device mismatch */
+  CBSPMV_EUNSUPPORTED = 6 /* e.g. device call on a host-only handle, blk != 16 on device */
+} cbspmv_status_t;
+
+typedef enum { CBSPMV_F64 = 0, CBSPMV_F32 = 1 } cbspmv_dtype_t;
+
+/* Sub-block storage formats. */
+enum { CBSPMV_FMT_COO = 0, CBSPMV_FMT_CSR = 1, CBSPMV_FMT_DENSE = 2 };
+
+typedef struct {
+  uint32_t struct_size;   /* sizeof(cbspmv_options_t); set by cbspmv_default_options */
+  int32_t blk;            /* sub-block edge, 16.  4 is accepted for host-only builds
+                             (the Fig. 1 fixture, R-21) */
+  int32_t th0_num;        /* th0 = th0_num / th0_den = 15/100; aggregate iff
+                             (#blocks with nnz < ss_limit) / (#non-empty blocks) >= th0 (R-3, R-5) */
+  int32_t th0_den;
+  int32_t ss_limit;       /* "super-sparse": nnz < 32 (R-4) */
+  int32_t th1, th2;       /* COO if nnz < th1, DENSE if nnz > th2, else CSR; 32 / 128 (R-9) */
+  int32_t warps_per_tb;   /* warp slots per thread block in Alg. 2, 8 */
+  int32_t agg_mode;       /* -1 decide by th0; 0 never; 1 always (ablation; global decision for shards) */
+  int32_t balance;        /* 1 = Alg. 2 TB-Load-Balance; 0 = natural (br,bc) order */
+  int32_t force_format;   /* -1 none; CBSPMV_FMT_* forces every block's format (white-box tests) */
+  int32_t device;         /* CUDA ordinal for the device copy; -1 = host-only build (export/info only) */
+  int32_t host_threads;   /* host builder threads; 0 = all online cores */
+  int32_t keep_host;      /* 1 = keep the canonical host arrays for cbspmv_export (default 1) */
+} cbspmv_options_t;
+
+typedef struct {
+  int64_t m, n, nnz;              /* nnz = stored non-zeros after dropping explicit zeros (R-19) */
+  int64_t blk_m;                  /* ceil(m / blk) block rows */
+  int64_t nb;                     /* non-empty sub-blocks after aggregation */
+  int64_t nb_pre;                 /* non-empty sub-blocks before aggregation */
+  int64_t ss_count;               /* super-sparse blocks before aggregation */
+  int32_t agg;                    /* column aggregation applied */
+  int32_t dtype;                  /* cbspmv_dtype_t */
+  int64_t fmt_count[3];           /* blocks per format (COO, CSR, DENSE) */
+  int64_t T;                      /* thread blocks = ceil(nb / warps_per_tb) (R-13) */
+  double tb_load_mean, tb_load_sd;          /* per-TB nnz after the schedule (Fig. 4) */
+  int64_t tb_load_max;
+  double tb_load_sd_natural;                /* per-TB nnz std-dev of the natural grouping */
+  int64_t tb_load_max_natural;
+  int64_t mtx_bytes;              /* |mtx_data| of the canonical packed format */
+  int64_t n_restore;              /* |restore_cols| (u32 each) */
+  int64_t meta_bytes;             /* 21 B per block: br, bc, nnz (i32), type (u8), vp (u64) */
+  int64_t alg_bytes;              /* algorithmic bytes of one SpMV: meta + mtx + 4*restore +
+                                     8*(blk_m+1 if agg) + size(Val)*(n + m) */
+  int64_t dev_stream_bytes;       /* bytes of the device page stream */
+  int64_t n_pages;                /* device pages */
+  int64_t dev_bytes;              /* all device memory owned by the handle */
+  int32_t grid;                   /* persistent CTAs per SpMV launch */
+  int32_t launches_per_spmv;      /* kernels launched by one cbspmv_spmv */
+  double build_seconds;           /* host pipeline wall time (a1..a7 + device layout) */
+  double upload_seconds;          /* H2D copy wall time */
+} cbspmv_info_t;
+
+/* Host copies of the canonical format, slot order (after Alg. 2).  Pointers
+ * are owned by the handle and valid until cbspmv_destroy. */
+typedef struct {
+  int64_t nb, T, mtx_bytes, n_restore, n_cols_offset;
+  const int32_t *blk_row_idx;     /* P:405 high-level COO over non-empty blocks */
+  const int32_t *blk_col_idx;     /* aggregated block column when agg (R-10) */
+  const int32_t *nnz_per_blk;
+  const uint8_t *type_per_blk;    /* CBSPMV_FMT_* */
+  const uint64_t *vp_per_blk;     /* byte offset of the block's record in mtx_data (R-11) */
+  const uint8_t *mtx_data;        /* packed records (R-8) */
+  const uint32_t *restore_cols;   /* aggregated -> original column, per block row */
+  const uint64_t *cols_offset;    /* blk_m + 1 entries when agg, else NULL (R-7) */
+  const int64_t *tb_ptr;          /* T + 1: blocks of TB t are [tb_ptr[t], tb_ptr[t+1]) (R-14) */
+  const int64_t *tb_load;         /* per-TB nnz after the schedule */
+  const int64_t *tb_load_natural; /* per-TB nnz of the natural grouping (pre-LB, Fig. 4) */
+} cbspmv_export_t;
+
+/* Fill *opts with the paper's defaults. */
+cbspmv_status_t cbspmv_default_options(cbspmv_options_t *opts);
+
+/* Build the CB-SpMV format of a host CSR matrix (the Fig. 7 pipeline):
+ * canonical check, 16x16 partition, th0 decision and block-aware
+ * column aggregation, format selection, intra-block data
+ * aggregation with virtual pointers and padding, TB-Load-Balance
+ * (Alg. 2); then lays the blocks out as the device page stream and
+ * uploads it in one copy ("transferred to the GPU in a single operation").
+ *   row_ptr: m+1 int64, non-decreasing, row_ptr[0] = 0
+ *   col_idx: nnz int32 in [0, n), strictly increasing within each row
+ *   vals:    nnz values of dtype (double or float); explicit zeros are dropped
+ *   opts:    NULL = defaults
+ *   stream:  stream for the upload; build returns after the upload completed
+ * The CSR is read during the call only.  On error *out is NULL. */
+cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr,
+                             const int32_t *col_idx, const void *vals, cbspmv_dtype_t dtype,
+                             const cbspmv_options_t *opts, void *stream, cbspmv_handle_t *out);
+
+/* y := A·x (Alg. 3 / Alg. 4 semantics).  Zeroes y, then one
+ * persistent kernel streams the page stream and adds every block's products
+ * into y (R-16).  x_dev: n values, y_dev: m values of the handle's dtype,
+ * 8-byte (f64) / 4-byte (f32) aligned, not aliasing. */
+cbspmv_status_t cbspmv_spmv(cbspmv_handle_t h, const void *x_dev, void *y_dev, void *stream);
+
+/* y += A·x (the kernel alone, no zeroing). */
+cbspmv_status_t cbspmv_spmv_add(cbspmv_handle_t h, const void *x_dev, void *y_dev, void *stream);
+
+/* y := A·(s·x) with s = 1/sqrt(*sumsq_dev) read on the device (power
+ * iteration: the normalisation of the previous iterate folded into the x load,
+ * SURVEY §8(e)).  sumsq_dev: one double on the device. */
+cbspmv_status_t cbspmv_spmv_scaled(cbspmv_handle_t h, const void *x_dev, const double *sumsq_dev,
+                                   void *y_dev, void *stream);
+
+/* End to end with host buffers: copies x_host (n values) to the device, runs
+ * cbspmv_spmv into an internal device y, copies y back to y_host (m values),
+ * and synchronises the stream before returning. */
+cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_host, void *stream);
+
+/* *out_dev (one double on the device) := sum_i v_i^2 over len values of dtype
+ * (the power-iteration finalize step). */
+cbspmv_status_t cbspmv_sumsq(const void *v_dev, int64_t len, cbspmv_dtype_t dtype, double *out_dev,
+                             int32_t device, void *stream);
+
+/* Steps a1 + a3 only (canonical check, then the block statistics th0 needs) for a
+ * host CSR, without building: *nb_pre = non-empty 16x16 blocks, *ss_count = blocks with
+ * nnz < ss_limit.  Row shards all-reduce these and pass the global decision
+ * (cbspmv_decide_agg) as agg_mode to cbspmv_build. */
+cbspmv_status_t cbspmv_block_stats(int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr,
+                                   const int32_t *col_idx, const void *vals, cbspmv_dtype_t dtype,
+                                   const cbspmv_options_t *opts, int64_t *nb_pre, int64_t *ss_count);
+
+/* *agg := 1 iff ss_count / nb_pre >= th0 (exact rational compare, R-3). */
+cbspmv_status_t cbspmv_decide_agg(int64_t nb_pre, int64_t ss_count, const cbspmv_options_t *opts,
+                                  int32_t *agg);
+
+cbspmv_status_t cbspmv_get_info(cbspmv_handle_t h, cbspmv_info_t *info);
+
+/* Canonical format (requires keep_host = 1). */
+cbspmv_status_t cbspmv_export(cbspmv_handle_t h, cbspmv_export_t *ex);
+
+/* Copy the device page stream (dev_stream_bytes) and page offsets
+ * (n_pages + 1 uint64) back to host buffers of at least that size (layout
+ * verification; synchronous). */
+cbspmv_status_t cbspmv_download_stream(cbspmv_handle_t h, void *stream_host, size_t stream_bytes,
+                                       uint64_t *page_off_host, size_t n_page_off);
+
+/* Free everything the handle owns.  NULL-safe. */
+cbspmv_status_t cbspmv_destroy(cbspmv_handle_t h);
+
+const char *cbspmv_status_string(cbspmv_status_t s);
+const char *cbspmv_last_error(void);
+int32_t cbspmv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBSPMV_H */

@@ -1,0 +1,286 @@
+"""B200-native CB-SpMV (arxiv 2605.18515): thin Python binding over ``libcbspmv.so``.
+
+Argument marshalling only — every step of the path (format build, load
+balance, device layout, SpMV) runs inside the C-ABI library declared in
+``include/cbspmv.h``.  There is no Python or CPU fallback: if the library is
+missing, importing the entry points raises.
+
+Names mirror the C ABI without the ``cbspmv_`` prefix::
+
+    h = build(A, dtype="f64", device=0)      # cbspmv_build (A: object with m, n, row_ptr, col, val)
+    spmv(h, x, y)                            # cbspmv_spmv         y := A x
+    spmv_add(h, x, y)                        # cbspmv_spmv_add     y += A x
+    spmv_scaled(h, x, sumsq, y)              # cbspmv_spmv_scaled  y := A (x / sqrt(sumsq))
+    spmv_host(h, x_np, y_np)                 # cbspmv_spmv_host    host buffers, end to end
+    sumsq(v, out)                            # cbspmv_sumsq
+    get_info(h), export(h), download_stream(h), destroy(h)
+
+Device vectors are torch CUDA tensors (or raw integer device pointers); the
+stream defaults to torch's current stream on the handle's device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcbspmv.so")
+_lib = None
+
+F64, F32 = 0, 1
+FMT_COO, FMT_CSR, FMT_DENSE = 0, 1, 2
+STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSORTED", 3: "ENOMEM", 4: "ECUDA", 5: "EDIM", 6: "EUNSUPPORTED"}
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32)] + [(k, ctypes.c_int32) for k in (
+        "blk", "th0_num", "th0_den", "ss_limit", "th1", "th2", "warps_per_tb", "agg_mode", "balance",
+        "force_format", "device", "host_threads", "keep_host")]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("blk_m", ctypes.c_int64),
+        ("nb", ctypes.c_int64), ("nb_pre", ctypes.c_int64), ("ss_count", ctypes.c_int64),
+        ("agg", ctypes.c_int32), ("dtype", ctypes.c_int32), ("fmt_count", ctypes.c_int64 * 3),
+        ("T", ctypes.c_int64), ("tb_load_mean", ctypes.c_double), ("tb_load_sd", ctypes.c_double),
+        ("tb_load_max", ctypes.c_int64), ("tb_load_sd_natural", ctypes.c_double),
+        ("tb_load_max_natural", ctypes.c_int64), ("mtx_bytes", ctypes.c_int64), ("n_restore", ctypes.c_int64),
+        ("meta_bytes", ctypes.c_int64), ("alg_bytes", ctypes.c_int64), ("dev_stream_bytes", ctypes.c_int64),
+        ("n_pages", ctypes.c_int64), ("dev_bytes", ctypes.c_int64), ("grid", ctypes.c_int32),
+        ("launches_per_spmv", ctypes.c_int32), ("build_seconds", ctypes.c_double),
+        ("upload_seconds", ctypes.c_double),
+    ]
+
+
+class Export(ctypes.Structure):
+    P = ctypes.POINTER
+    _fields_ = [
+        ("nb", ctypes.c_int64), ("T", ctypes.c_int64), ("mtx_bytes", ctypes.c_int64),
+        ("n_restore", ctypes.c_int64), ("n_cols_offset", ctypes.c_int64),
+        ("blk_row_idx", P(ctypes.c_int32)), ("blk_col_idx", P(ctypes.c_int32)), ("nnz_per_blk", P(ctypes.c_int32)),
+        ("type_per_blk", P(ctypes.c_uint8)), ("vp_per_blk", P(ctypes.c_uint64)), ("mtx_data", P(ctypes.c_uint8)),
+        ("restore_cols", P(ctypes.c_uint32)), ("cols_offset", P(ctypes.c_uint64)), ("tb_ptr", P(ctypes.c_int64)),
+        ("tb_load", P(ctypes.c_int64)), ("tb_load_natural", P(ctypes.c_int64)),
+    ]
+
+
+def lib():
+    """Load libcbspmv.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `make -C {os.path.dirname(_HERE)} lib` "
+                               "(no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, vp, i32 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32
+        H = ctypes.c_void_p
+        sig = {
+            "cbspmv_default_options": ([ctypes.POINTER(Options)], i32),
+            "cbspmv_build": ([i64, i64, i64, vp, vp, vp, i32, ctypes.POINTER(Options), vp, ctypes.POINTER(H)], i32),
+            "cbspmv_spmv": ([H, vp, vp, vp], i32),
+            "cbspmv_spmv_add": ([H, vp, vp, vp], i32),
+            "cbspmv_spmv_scaled": ([H, vp, vp, vp, vp], i32),
+            "cbspmv_spmv_host": ([H, vp, vp, vp], i32),
+            "cbspmv_sumsq": ([vp, i64, i32, vp, i32, vp], i32),
+            "cbspmv_block_stats": ([i64, i64, i64, vp, vp, vp, i32, ctypes.POINTER(Options),
+                                    ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+            "cbspmv_decide_agg": ([i64, i64, ctypes.POINTER(Options), ctypes.POINTER(i32)], i32),
+            "cbspmv_get_info": ([H, ctypes.POINTER(Info)], i32),
+            "cbspmv_export": ([H, ctypes.POINTER(Export)], i32),
+            "cbspmv_download_stream": ([H, vp, ctypes.c_size_t, vp, ctypes.c_size_t], i32),
+            "cbspmv_destroy": ([H], i32),
+            "cbspmv_status_string": ([i32], ctypes.c_char_p),
+            "cbspmv_last_error": ([], ctypes.c_char_p),
+            "cbspmv_version": ([], i32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+class CBSpMVError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        detail = lib().cbspmv_last_error().decode()
+        super().__init__(f"{what}: {STATUS.get(status, status)} ({detail})")
+        self.status = status
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise CBSpMVError(st, what)
+
+
+def default_options(**kw) -> Options:
+    o = Options()
+    _check(lib().cbspmv_default_options(ctypes.byref(o)), "cbspmv_default_options")
+    for k, v in kw.items():
+        if not hasattr(o, k) or k == "struct_size":
+            raise KeyError(k)
+        setattr(o, k, int(v))
+    return o
+
+
+def _ptr(t) -> int | None:
+    """Device pointer of a torch tensor (or an int pointer) — marshalling only."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return t.data_ptr()
+    raise TypeError(type(t))
+
+
+def _stream(stream, device: int) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream(device).cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Handle:
+    """Owns one cbspmv_handle_t (a built matrix, or a row shard of one)."""
+
+    def __init__(self, raw: ctypes.c_void_p, dtype: int, device: int):
+        self._raw = raw
+        self.dtype = dtype
+        self.device = device
+        self.info = get_info(self)
+
+    @property
+    def raw(self):
+        if self._raw is None:
+            raise ValueError("handle destroyed")
+        return self._raw
+
+    def __del__(self):
+        try:
+            destroy(self)
+        except Exception:
+            pass
+
+
+def build(A, dtype: str | int = "f64", device: int = 0, stream=None, **opts) -> Handle:
+    """cbspmv_build on a host CSR (``A.m, A.n, A.row_ptr, A.col, A.val``)."""
+    dt = {"f64": F64, "f32": F32, F64: F64, F32: F32}[dtype]
+    o = default_options(device=device, **opts)
+    rp = np.ascontiguousarray(A.row_ptr, np.int64)
+    col = np.ascontiguousarray(A.col, np.int32)
+    val = np.ascontiguousarray(A.val, np.float64 if dt == F64 else np.float32)
+    h = ctypes.c_void_p()
+    st = None
+    if device >= 0:
+        st = _stream(stream, device)
+    _check(lib().cbspmv_build(A.m, A.n, int(rp[-1]) if len(rp) else 0, rp.ctypes.data, col.ctypes.data,
+                              val.ctypes.data, dt, ctypes.byref(o), st, ctypes.byref(h)), "cbspmv_build")
+    return Handle(h, dt, device)
+
+
+def block_stats(A, dtype: str | int = "f64", **opts) -> tuple[int, int]:
+    """cbspmv_block_stats: (non-empty blocks, super-sparse blocks) before aggregation."""
+    dt = {"f64": F64, "f32": F32, F64: F64, F32: F32}[dtype]
+    o = default_options(**opts)
+    rp = np.ascontiguousarray(A.row_ptr, np.int64)
+    col = np.ascontiguousarray(A.col, np.int32)
+    val = np.ascontiguousarray(A.val, np.float64 if dt == F64 else np.float32)
+    nb, ss = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().cbspmv_block_stats(A.m, A.n, int(rp[-1]) if len(rp) else 0, rp.ctypes.data, col.ctypes.data,
+                                    val.ctypes.data, dt, ctypes.byref(o), ctypes.byref(nb), ctypes.byref(ss)),
+           "cbspmv_block_stats")
+    return nb.value, ss.value
+
+
+def decide_agg(nb_pre: int, ss_count: int, **opts) -> int:
+    """cbspmv_decide_agg: the th0 rule on (possibly all-reduced) block statistics."""
+    o = default_options(**opts)
+    a = ctypes.c_int32()
+    _check(lib().cbspmv_decide_agg(int(nb_pre), int(ss_count), ctypes.byref(o), ctypes.byref(a)), "cbspmv_decide_agg")
+    return a.value
+
+
+def spmv(h: Handle, x, y, stream=None) -> None:
+    _check(lib().cbspmv_spmv(h.raw, _ptr(x), _ptr(y), _stream(stream, h.device)), "cbspmv_spmv")
+
+
+def spmv_add(h: Handle, x, y, stream=None) -> None:
+    _check(lib().cbspmv_spmv_add(h.raw, _ptr(x), _ptr(y), _stream(stream, h.device)), "cbspmv_spmv_add")
+
+
+def spmv_scaled(h: Handle, x, sumsq_dev, y, stream=None) -> None:
+    _check(lib().cbspmv_spmv_scaled(h.raw, _ptr(x), _ptr(sumsq_dev), _ptr(y), _stream(stream, h.device)),
+           "cbspmv_spmv_scaled")
+
+
+def spmv_host(h: Handle, x: np.ndarray, y: np.ndarray, stream=None) -> None:
+    vt = np.float64 if h.dtype == F64 else np.float32
+    if x.dtype != vt or y.dtype != vt or not x.flags.c_contiguous or not y.flags.c_contiguous:
+        raise ValueError("host x / y must be contiguous arrays of the handle's dtype")
+    if x.size != h.info["n"] or y.size != h.info["m"]:
+        raise ValueError("size mismatch")
+    _check(lib().cbspmv_spmv_host(h.raw, x.ctypes.data, y.ctypes.data, _stream(stream, h.device)),
+           "cbspmv_spmv_host")
+
+
+def sumsq(v, out, device: int = 0, stream=None) -> None:
+    dt = F64 if str(v.dtype).endswith("float64") else F32
+    _check(lib().cbspmv_sumsq(_ptr(v), v.numel(), dt, _ptr(out), device, _stream(stream, device)), "cbspmv_sumsq")
+
+
+def get_info(h: Handle) -> dict:
+    i = Info()
+    _check(lib().cbspmv_get_info(h.raw, ctypes.byref(i)), "cbspmv_get_info")
+    d = {k: getattr(i, k) for k, _ in Info._fields_}
+    d["fmt_count"] = tuple(i.fmt_count)
+    return d
+
+
+def export(h: Handle) -> dict:
+    """Host copies of the canonical format (slot order) as numpy arrays."""
+    e = Export()
+    _check(lib().cbspmv_export(h.raw, ctypes.byref(e)), "cbspmv_export")
+
+    def arr(p, n, dt):
+        if n == 0 or not p:
+            return np.zeros(0, dt)
+        return np.ctypeslib.as_array(p, shape=(n,)).copy()
+
+    nb, T = e.nb, e.T
+    return dict(
+        nb=nb, T=T,
+        blk_row_idx=arr(e.blk_row_idx, nb, np.int32), blk_col_idx=arr(e.blk_col_idx, nb, np.int32),
+        nnz_per_blk=arr(e.nnz_per_blk, nb, np.int32), type_per_blk=arr(e.type_per_blk, nb, np.uint8),
+        vp_per_blk=arr(e.vp_per_blk, nb, np.uint64), mtx_data=arr(e.mtx_data, e.mtx_bytes, np.uint8),
+        restore_cols=arr(e.restore_cols, e.n_restore, np.uint32),
+        cols_offset=arr(e.cols_offset, e.n_cols_offset, np.uint64),
+        tb_ptr=arr(e.tb_ptr, T + 1, np.int64), tb_load=arr(e.tb_load, T, np.int64),
+        tb_load_natural=arr(e.tb_load_natural, T, np.int64),
+    )
+
+
+def download_stream(h: Handle) -> tuple[np.ndarray, np.ndarray]:
+    nbytes, npages = h.info["dev_stream_bytes"], h.info["n_pages"]
+    s = np.zeros(max(nbytes, 1), np.uint8)
+    po = np.zeros(npages + 1, np.uint64)
+    _check(lib().cbspmv_download_stream(h.raw, s.ctypes.data, s.size, po.ctypes.data, po.size),
+           "cbspmv_download_stream")
+    return s[:nbytes], po
+
+
+def destroy(h: Handle) -> None:
+    if h._raw is not None:
+        lib().cbspmv_destroy(h._raw)
+        h._raw = None
+
+
+def version() -> int:
+    return lib().cbspmv_version()

@@ -1,0 +1,488 @@
+// builder.cpp — host format builder of CB-SpMV (the Fig. 7 pipeline),
+// multi-threaded C++17.  Produces the canonical format byte-identical to the
+// paper-literal oracle (tests/test_builder_parity.py) and the derived device
+// page stream.
+//
+// Steps:
+//   a1 canonical check + explicit-zero drop (R-19)
+//   a2 partition into BxB sub-blocks, block-COO in (br, bc) order
+//   a3 super-sparse fraction and the th0 decision (R-3..R-5)
+//   a4 block-aware column aggregation per block row (R-6, R-7)
+//   a5 format selection COO / CSR / DENSE (R-9, R-10)
+//   a6 intra-block data aggregation: records, VP, padding (R-8, R-11)
+//   a7 TB-Load-Balance, Alg. 2 (R-12..R-14), as a counting sort plus a
+//      bucket queue keyed by (load, tb_id) — the same pop order as a binary min-heap.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <thread>
+
+#include "cb_internal.h"
+
+#include <cuda_runtime.h>
+
+namespace cb {
+
+int resolve_threads(int t) {
+  if (t > 0) return t;
+  unsigned h = std::thread::hardware_concurrency();
+  return h ? (int)std::min(h, 128u) : 1;
+}
+
+void parallel_for(int64_t n, int threads, int64_t grain, const std::function<void(int64_t, int64_t, int)> &fn) {
+  if (n <= 0) return;
+  threads = resolve_threads(threads);
+  if (threads == 1 || n <= grain) { fn(0, n, 0); return; }
+  std::atomic<int64_t> next{0};
+  auto worker = [&](int tid) {
+    for (;;) {
+      int64_t lo = next.fetch_add(grain);
+      if (lo >= n) break;
+      fn(lo, std::min(n, lo + grain), tid);
+    }
+  };
+  std::vector<std::thread> th;
+  int T = (int)std::min<int64_t>(threads, (n + grain - 1) / grain);
+  for (int t = 1; t < T; t++) th.emplace_back(worker, t);
+  worker(0);
+  for (auto &x : th) x.join();
+}
+
+namespace {
+
+inline double get_val(const Csr &A, int64_t j) {
+  return A.val_size == 8 ? ((const double *)A.val)[j] : (double)((const float *)A.val)[j];
+}
+
+// Element of one block row, sortable by (block column, local row, local column).
+struct Key {
+  uint64_t key;  // bcol << 8 | lr << 4 | lc
+  int64_t j;     // CSR position of the value
+  bool operator<(const Key &o) const { return key < o.key; }
+};
+
+// Per-thread scratch reused across block rows.
+struct Scratch {
+  std::vector<Key> keys;
+  std::vector<uint32_t> cols;
+};
+
+// Collect the block row's non-zeros as keys; with aggregation, columns are replaced by their
+// rank in C_i (sorted distinct columns of the block row) and C_i is left in s.cols.
+void block_row_keys(const Csr &A, int B, int64_t br, bool agg, Scratch &s) {
+  s.keys.clear();
+  int64_t r0 = br * B, r1 = std::min<int64_t>(A.m, r0 + B);
+  if (agg) {
+    s.cols.clear();
+    for (int64_t r = r0; r < r1; r++)
+      for (int64_t j = A.row_ptr[r]; j < A.row_ptr[r + 1]; j++)
+        if (get_val(A, j) != 0.0) s.cols.push_back((uint32_t)A.col[j]);
+    std::sort(s.cols.begin(), s.cols.end());
+    s.cols.erase(std::unique(s.cols.begin(), s.cols.end()), s.cols.end());
+  }
+  for (int64_t r = r0; r < r1; r++) {
+    uint64_t lr = (uint64_t)(r - r0);
+    const uint32_t *cb = s.cols.data(), *ce = cb + s.cols.size(), *cur = cb;
+    for (int64_t j = A.row_ptr[r]; j < A.row_ptr[r + 1]; j++) {
+      if (get_val(A, j) == 0.0) continue;
+      uint64_t c = (uint64_t)A.col[j];
+      if (agg) {  // columns of a row are increasing: advance the rank cursor monotonically
+        cur = std::lower_bound(cur, ce, (uint32_t)c);
+        c = (uint64_t)(cur - cb);
+      }
+      s.keys.push_back({((c / B) << 8) | (lr << 4) | (c % B), j});
+    }
+  }
+  std::sort(s.keys.begin(), s.keys.end());
+}
+
+inline int64_t padding(int64_t idx_bytes, int64_t S) {  // Alg. 3 lines 6-7
+  int64_t p = idx_bytes % S;
+  return p ? S - p : 0;
+}
+
+inline int select_format(int64_t nnz, const cbspmv_options_t &o) {  // P:439 (R-9)
+  if (o.force_format >= 0) return o.force_format;
+  if (nnz < o.th1) return CBSPMV_FMT_COO;
+  if (nnz > o.th2) return CBSPMV_FMT_DENSE;
+  return CBSPMV_FMT_CSR;
+}
+
+inline int64_t record_bytes(int type, int64_t nnz, int B, int64_t S) {  // a6 (R-8)
+  int64_t idx = type == CBSPMV_FMT_COO ? nnz : type == CBSPMV_FMT_CSR ? (B + 1) + nnz : 0;
+  int64_t nval = type == CBSPMV_FMT_DENSE ? (int64_t)B * B : nnz;
+  return idx + padding(idx, S) + nval * S;
+}
+
+inline void put_val(uint8_t *dst, int64_t i, double v, int64_t S) {
+  if (S == 8) std::memcpy(dst + 8 * i, &v, 8);
+  else { float f = (float)v; std::memcpy(dst + 4 * i, &f, 4); }
+}
+
+// Pack one block's record at dst (zero-filled); e = its keys (sorted), k = nnz.
+void pack_record(const Csr &A, int B, int64_t S, int type, const Key *e, int64_t k, uint8_t *dst) {
+  if (type == CBSPMV_FMT_COO) {
+    for (int64_t t = 0; t < k; t++) {
+      uint32_t lr = (e[t].key >> 4) & 15, lc = e[t].key & 15;
+      dst[t] = (uint8_t)((lc << 4) | lr);  // row = b & 15, col = b >> 4
+    }
+    uint8_t *vals = dst + k + padding(k, S);
+    for (int64_t t = 0; t < k; t++) put_val(vals, t, get_val(A, e[t].j), S);
+  } else if (type == CBSPMV_FMT_CSR) {
+    int64_t t = 0;
+    for (int r = 0; r <= B; r++) {
+      while (t < k && (int)((e[t].key >> 4) & 15) < r) t++;
+      dst[r] = (uint8_t)(t & 0xFF);
+    }
+    for (int64_t q = 0; q < k; q++) dst[B + 1 + q] = (uint8_t)(e[q].key & 15);
+    uint8_t *vals = dst + (B + 1) + k + padding((B + 1) + k, S);
+    for (int64_t q = 0; q < k; q++) put_val(vals, q, get_val(A, e[q].j), S);
+  } else {
+    for (int64_t q = 0; q < k; q++) {
+      int64_t pos = (int64_t)((e[q].key >> 4) & 15) * B + (int64_t)(e[q].key & 15);
+      put_val(dst, pos, get_val(A, e[q].j), S);
+    }
+  }
+}
+
+}  // namespace
+
+namespace {
+
+int check_options(const Csr &A, const cbspmv_options_t &o, std::string *err) {
+  const int B = o.blk, W = o.warps_per_tb;
+  if (A.m < 0 || A.n < 0 || A.n > INT32_MAX || (B != 16 && B != 4) || W < 1 || W > 1024 ||
+      (A.val_size != 4 && A.val_size != 8) || o.th0_den <= 0 || o.force_format < -1 || o.force_format > 2) {
+    *err = "invalid dimensions or options";
+    return CBSPMV_EINVAL;
+  }
+  if (A.m > 0 && (!A.row_ptr || (A.row_ptr[A.m] > 0 && (!A.col || !A.val)))) {
+    *err = "null CSR array";
+    return CBSPMV_EINVAL;
+  }
+  if (A.m > 0 && (A.row_ptr[0] != 0 || A.row_ptr[A.m] != A.nnz)) {
+    *err = "row_ptr[0] must be 0 and row_ptr[m] must equal nnz";
+    return CBSPMV_EINVAL;
+  }
+  return CBSPMV_OK;
+}
+
+// a1. canonical check; the first violation in row-major order decides the status (as a
+// sequential scan would).  *nnz = stored non-zeros after dropping explicit zeros.
+int canonical_check(const Csr &A, int threads, int64_t *nnz, std::string *err) {
+  const int T = resolve_threads(threads);
+  struct Fail { int64_t pos = INT64_MAX; int code = 0; int64_t row = -1; };
+  std::vector<Fail> fails(T);
+  std::vector<int64_t> part(T, 0);
+  parallel_for(A.m, T, 1 << 14, [&](int64_t lo, int64_t hi, int tid) {
+    Fail &f = fails[tid];
+    int64_t acc = 0;
+    for (int64_t i = lo; i < hi; i++) {
+      int64_t b = A.row_ptr[i], e = A.row_ptr[i + 1];
+      if (e < b) { if (b < f.pos) { f.pos = b; f.code = CBSPMV_EINVAL; f.row = i; } continue; }
+      for (int64_t j = b; j < e; j++) {
+        int code = 0;
+        if (A.col[j] < 0 || A.col[j] >= A.n) code = CBSPMV_EINVAL;
+        else if (j > b && A.col[j] <= A.col[j - 1]) code = CBSPMV_EUNSORTED;
+        else if (!std::isfinite(get_val(A, j))) code = CBSPMV_EINVAL;
+        if (code) { if (j < f.pos) { f.pos = j; f.code = code; f.row = i; } break; }
+        if (get_val(A, j) != 0.0) acc++;
+      }
+    }
+    part[tid] += acc;
+  });
+  Fail first;
+  for (auto &f : fails) if (f.pos < first.pos) first = f;
+  if (first.code) {
+    *err = (first.code == CBSPMV_EUNSORTED ? "columns not strictly increasing in row "
+                                           : "invalid entry (column out of range or non-finite) in row ") +
+           std::to_string(first.row);
+    return first.code;
+  }
+  *nnz = 0;
+  for (int64_t v : part) *nnz += v;
+  return CBSPMV_OK;
+}
+
+// a3. block statistics before aggregation: #non-empty blocks, #super-sparse blocks.
+void pre_stats(const Csr &A, const cbspmv_options_t &o, int64_t blk_m, std::vector<Scratch> &scr,
+               int64_t *nb_pre, int64_t *ss_count) {
+  std::vector<int64_t> pre_nb(blk_m), pre_ss(blk_m);
+  parallel_for(blk_m, (int)scr.size(), 64, [&](int64_t lo, int64_t hi, int tid) {
+    Scratch &s = scr[tid];
+    for (int64_t br = lo; br < hi; br++) {
+      block_row_keys(A, o.blk, br, false, s);
+      int64_t nb = 0, ss = 0, run = 0;
+      for (size_t t = 0; t < s.keys.size(); t++) {
+        run++;
+        if (t + 1 == s.keys.size() || (s.keys[t + 1].key >> 8) != (s.keys[t].key >> 8)) {
+          nb++; ss += run < o.ss_limit; run = 0;
+        }
+      }
+      pre_nb[br] = nb; pre_ss[br] = ss;
+    }
+  });
+  *nb_pre = 0; *ss_count = 0;
+  for (int64_t br = 0; br < blk_m; br++) { *nb_pre += pre_nb[br]; *ss_count += pre_ss[br]; }
+}
+
+}  // namespace
+
+bool decide_agg(int64_t nb_pre, int64_t ss_count, const cbspmv_options_t &o) {
+  // aggregate iff ss / nb >= th0_num / th0_den, compared exactly in integers (R-3, R-5)
+  return nb_pre > 0 && ss_count * (int64_t)o.th0_den >= (int64_t)o.th0_num * nb_pre;
+}
+
+int block_stats(const Csr &A, const cbspmv_options_t &o, int64_t *nb_pre, int64_t *ss_count, std::string *err) {
+  int st = check_options(A, o, err);
+  if (st != CBSPMV_OK) return st;
+  int64_t nnz = 0;
+  st = canonical_check(A, o.host_threads, &nnz, err);
+  if (st != CBSPMV_OK) return st;
+  std::vector<Scratch> scr(resolve_threads(o.host_threads));
+  pre_stats(A, o, (A.m + o.blk - 1) / o.blk, scr, nb_pre, ss_count);
+  return CBSPMV_OK;
+}
+
+int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::string *err) {
+  const int B = o.blk, W = o.warps_per_tb, threads = o.host_threads;
+  const int64_t S = A.val_size;
+  int st = check_options(A, o, err);
+  if (st != CBSPMV_OK) return st;
+  Canon &c = *out;
+  c = Canon();
+  c.m = A.m; c.n = A.n; c.blk = B; c.val_size = (int)S; c.W = W;
+  c.blk_m = (A.m + B - 1) / B;
+  st = canonical_check(A, threads, &c.nnz, err);   // a1
+  if (st != CBSPMV_OK) return st;
+  const int T = resolve_threads(threads);
+  std::vector<Scratch> scr(T);
+  pre_stats(A, o, c.blk_m, scr, &c.nb_pre, &c.ss_count);   // a3
+  c.agg = o.agg_mode >= 0 ? o.agg_mode : decide_agg(c.nb_pre, c.ss_count, o);
+  const bool agg = c.agg != 0;
+
+  // a4 + a5 sizing pass: blocks, restore entries and record bytes per block row.
+  std::vector<int64_t> br_nb(c.blk_m + 1, 0), br_res(c.blk_m + 1, 0), br_bytes(c.blk_m + 1, 0);
+  parallel_for(c.blk_m, T, 64, [&](int64_t lo, int64_t hi, int tid) {
+    Scratch &s = scr[tid];
+    for (int64_t br = lo; br < hi; br++) {
+      block_row_keys(A, B, br, agg, s);
+      int64_t nb = 0, bytes = 0, run = 0;
+      for (size_t t = 0; t < s.keys.size(); t++) {
+        run++;
+        if (t + 1 == s.keys.size() || (s.keys[t + 1].key >> 8) != (s.keys[t].key >> 8)) {
+          nb++; bytes += record_bytes(select_format(run, o), run, B, S); run = 0;
+        }
+      }
+      br_nb[br + 1] = nb; br_res[br + 1] = agg ? (int64_t)s.cols.size() : 0; br_bytes[br + 1] = bytes;
+    }
+  });
+  for (int64_t br = 0; br < c.blk_m; br++) {
+    br_nb[br + 1] += br_nb[br]; br_res[br + 1] += br_res[br]; br_bytes[br + 1] += br_bytes[br];
+  }
+  const int64_t nb = br_nb[c.blk_m];
+  c.nb = nb;
+  c.mtx.assign((size_t)br_bytes[c.blk_m], 0);
+  if (agg) {
+    c.restore.resize((size_t)br_res[c.blk_m]);
+    c.cols_offset.resize((size_t)c.blk_m + 1);
+    for (int64_t br = 0; br <= c.blk_m; br++) c.cols_offset[br] = (uint64_t)br_res[br];
+  }
+
+  // a6 fill pass: natural-order metadata, restore_cols, packed records at VP = byte offset.
+  std::vector<int32_t> nbr(nb), nbc(nb), nnzb(nb);
+  std::vector<uint8_t> ntype(nb);
+  std::vector<uint64_t> nvp(nb);
+  parallel_for(c.blk_m, T, 64, [&](int64_t lo, int64_t hi, int tid) {
+    Scratch &s = scr[tid];
+    for (int64_t br = lo; br < hi; br++) {
+      block_row_keys(A, B, br, agg, s);
+      if (agg) std::copy(s.cols.begin(), s.cols.end(), c.restore.begin() + br_res[br]);
+      int64_t b = br_nb[br], off = br_bytes[br], start = 0;
+      for (size_t t = 0; t < s.keys.size(); t++) {
+        if (t + 1 == s.keys.size() || (s.keys[t + 1].key >> 8) != (s.keys[t].key >> 8)) {
+          int64_t k = (int64_t)t + 1 - start;
+          int type = select_format(k, o);
+          nbr[b] = (int32_t)br; nbc[b] = (int32_t)(s.keys[t].key >> 8); nnzb[b] = (int32_t)k;
+          ntype[b] = (uint8_t)type; nvp[b] = (uint64_t)off;
+          pack_record(A, B, S, type, &s.keys[start], k, c.mtx.data() + off);
+          off += record_bytes(type, k, B, S);
+          b++; start = (int64_t)t + 1;
+        }
+      }
+    }
+  });
+  for (int64_t b = 0; b < nb; b++) c.fmt_count[ntype[b]]++;
+
+  // a7. TB-Load-Balance (Alg. 2).
+  const int64_t TB = (nb + W - 1) / W;
+  c.T = TB;
+  c.tb_ptr.assign((size_t)TB + 1, 0);
+  c.tb_load.assign((size_t)TB, 0);
+  c.tb_load_nat.assign((size_t)TB, 0);
+  for (int64_t b = 0; b < nb; b++) c.tb_load_nat[b / W] += nnzb[b];
+  std::vector<int64_t> perm(nb);  // slot-order position -> natural block index
+  if (o.balance && nb > 0) {
+    // "parallel sort(blk_idx_array, cmp_nnz)": nnz descending, ties by index ascending (R-12);
+    // a stable counting sort over nnz in [1, B*B].
+    const int maxk = B * B;
+    std::vector<int64_t> cnt(maxk + 2, 0);
+    for (int64_t b = 0; b < nb; b++) cnt[maxk - nnzb[b]]++;
+    int64_t acc = 0;
+    for (int k = 0; k <= maxk; k++) { int64_t t = cnt[k]; cnt[k] = acc; acc += t; }
+    std::vector<int64_t> order(nb);
+    for (int64_t b = 0; b < nb; b++) order[cnt[maxk - nnzb[b]]++] = b;
+    // min-heap over (loads, tb_id) as a bucket queue: loads <= W*B*B, and the minimum load
+    // never decreases (each pop re-pushes with a larger load), so a forward cursor suffices.
+    const int64_t maxload = (int64_t)W * maxk;
+    std::vector<std::vector<uint32_t>> bucket((size_t)maxload + 1);
+    bucket[0].resize((size_t)TB);
+    for (int64_t t = 0; t < TB; t++) bucket[0][t] = (uint32_t)t;  // ascending = a valid min-heap
+    std::vector<int32_t> warps(TB, 0);
+    std::vector<uint32_t> slot_tb(nb);
+    std::vector<int32_t> slot_w(nb);
+    int64_t cur = 0;
+    auto gt = std::greater<uint32_t>();
+    for (int64_t i = 0; i < nb; i++) {
+      while (bucket[cur].empty()) cur++;
+      std::vector<uint32_t> &bk = bucket[cur];
+      std::pop_heap(bk.begin(), bk.end(), gt);
+      uint32_t tb = bk.back();
+      bk.pop_back();
+      int64_t b = order[i];
+      slot_tb[b] = tb; slot_w[b] = warps[tb];        // end <- tb_id*8 + warps
+      c.tb_load[tb] += nnzb[b];                      // loads <- loads + nnz
+      warps[tb]++;                                   // warps <- warps + 1
+      if (warps[tb] < W) {                           // if warps < 8: push
+        std::vector<uint32_t> &nbk = bucket[(size_t)c.tb_load[tb]];
+        nbk.push_back(tb);
+        std::push_heap(nbk.begin(), nbk.end(), gt);
+      }
+    }
+    // "parallel sort(blk_idx_array, cmp_end)": ends are unique, so position = tb_ptr[tb] + w.
+    for (int64_t t = 0; t < TB; t++) c.tb_ptr[t + 1] = c.tb_ptr[t] + warps[t];
+    for (int64_t b = 0; b < nb; b++) perm[c.tb_ptr[slot_tb[b]] + slot_w[b]] = b;
+  } else {
+    for (int64_t b = 0; b < nb; b++) perm[b] = b;
+    for (int64_t t = 0; t < TB; t++) {
+      c.tb_ptr[t + 1] = std::min<int64_t>(nb, (t + 1) * W);
+      c.tb_load[t] = c.tb_load_nat[t];
+    }
+  }
+  // permute the five high-level arrays (vp_per_blk[i] <- vp_per_blk_old[ori])
+  c.br.resize(nb); c.bc.resize(nb); c.nnzb.resize(nb); c.type.resize(nb); c.vp.resize(nb);
+  parallel_for(nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t i = lo; i < hi; i++) {
+      int64_t b = perm[i];
+      c.br[i] = nbr[b]; c.bc[i] = nbc[b]; c.nnzb[i] = nnzb[b]; c.type[i] = ntype[b]; c.vp[i] = nvp[b];
+    }
+  });
+  return CBSPMV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device page stream
+// ---------------------------------------------------------------------------
+static inline int64_t dev_record_bytes(const Canon &c, int64_t i, int64_t canon_bytes, int *ncols_out) {
+  int ncols;
+  if (c.agg) {
+    int64_t w = (int64_t)(c.cols_offset[c.br[i] + 1] - c.cols_offset[c.br[i]]) - (int64_t)c.bc[i] * c.blk;
+    ncols = (int)std::min<int64_t>(c.blk, w);
+  } else {
+    ncols = (int)std::min<int64_t>(c.blk, c.n - (int64_t)c.bc[i] * c.blk);
+  }
+  *ncols_out = ncols;
+  int64_t restore_bytes = c.agg ? round_up(ncols, 4) * 4 : 0;
+  return round_up(restore_bytes + canon_bytes, 16);
+}
+
+static inline int64_t canon_record_bytes(const Canon &c, int64_t i) {
+  int64_t B = c.blk, S = c.val_size, k = c.nnzb[i];
+  int type = c.type[i];
+  int64_t idx = type == CBSPMV_FMT_COO ? k : type == CBSPMV_FMT_CSR ? (B + 1) + k : 0;
+  int64_t nval = type == CBSPMV_FMT_DENSE ? B * B : k;
+  int64_t p = idx % S;
+  return idx + (p ? S - p : 0) + nval * S;
+}
+
+void free_stream(Stream *s) {
+  if (s->bytes) {
+    if (s->pinned) cudaFreeHost(s->bytes);
+    else std::free(s->bytes);
+  }
+  s->bytes = nullptr; s->nbytes = 0; s->page_off.clear();
+}
+
+int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::string *err) {
+  const int T = resolve_threads(threads);
+  std::vector<int64_t> rec(c.nb);
+  std::vector<int32_t> ncol(c.nb);
+  parallel_for(c.nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t i = lo; i < hi; i++) { int nc; rec[i] = dev_record_bytes(c, i, canon_record_bytes(c, i), &nc); ncol[i] = nc; }
+  });
+  // Greedy pages of whole thread blocks (slot order), each <= page_cap bytes.
+  std::vector<int64_t> page_tb;  // first TB of each page
+  std::vector<uint64_t> off;
+  int64_t total = 0, cur = -1;
+  int64_t cur_bytes = 0;
+  for (int64_t t = 0; t < c.T; t++) {
+    int64_t tb_bytes = 0;
+    for (int64_t i = c.tb_ptr[t]; i < c.tb_ptr[t + 1]; i++) tb_bytes += kDescBytes + rec[i];
+    if (kPageHeader + tb_bytes > page_cap) {
+      *err = "page capacity too small for one thread block";
+      return CBSPMV_EINVAL;
+    }
+    if (cur < 0 || cur_bytes + tb_bytes > page_cap) {
+      if (cur >= 0) total += round_up(cur_bytes, 16);
+      page_tb.push_back(t); off.push_back((uint64_t)total);
+      cur = t; cur_bytes = kPageHeader;
+    }
+    cur_bytes += tb_bytes;
+  }
+  if (cur >= 0) total += round_up(cur_bytes, 16);
+  off.push_back((uint64_t)total);
+  page_tb.push_back(c.T);
+  const int64_t npages = (int64_t)off.size() - 1;
+
+  s->nbytes = total;
+  s->page_off = off;
+  if (total > 0) {
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, (size_t)total, cudaHostAllocDefault) == cudaSuccess) s->pinned = true;
+    else { cudaGetLastError(); p = std::malloc((size_t)total); s->pinned = false; }
+    if (!p) { *err = "host allocation of the page stream failed"; return CBSPMV_ENOMEM; }
+    s->bytes = (uint8_t *)p;
+  }
+  parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t p = lo; p < hi; p++) {
+      uint8_t *page = s->bytes + off[p];
+      int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
+      int64_t nblk = b1 - b0;
+      std::memset(page, 0, (size_t)(off[p + 1] - off[p]));
+      uint32_t hdr[4] = {(uint32_t)nblk, (uint32_t)page_tb[p], (uint32_t)(page_tb[p + 1] - page_tb[p]), 0};
+      std::memcpy(page, hdr, 16);
+      int64_t pos = kPageHeader + kDescBytes * nblk;  // already a multiple of 16
+      for (int64_t i = b0; i < b1; i++) {
+        Desc d;
+        d.row0 = (uint32_t)c.br[i] * (uint32_t)c.blk;
+        d.xcol0 = c.agg ? 0u : (uint32_t)c.bc[i] * (uint32_t)c.blk;
+        d.w2 = pack_w2((uint32_t)(pos / 16), (uint32_t)c.nnzb[i], c.type[i]);
+        d.ncols = (uint32_t)ncol[i];
+        std::memcpy(page + kPageHeader + kDescBytes * (i - b0), &d, sizeof(d));
+        uint8_t *r = page + pos;
+        if (c.agg) {
+          const uint32_t *seg = c.restore.data() + c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk;
+          std::memcpy(r, seg, (size_t)ncol[i] * 4);
+          r += round_up(ncol[i], 4) * 4;
+        }
+        std::memcpy(r, c.mtx.data() + c.vp[i], (size_t)canon_record_bytes(c, i));
+        pos += rec[i];
+      }
+    }
+  });
+  return CBSPMV_OK;
+}
+
+}  // namespace cb

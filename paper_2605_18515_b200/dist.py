@@ -1,0 +1,90 @@
+"""Row sharding across GPUs — plumbing around the C ABI.
+
+* ``shard_bounds`` cuts the rows at 16-row block-row boundaries by prefix-summed
+  nnz: cut k is the first block row whose cumulative nnz reaches k*nnz/P.
+  Block rows are independent units of the method (no block spans two block
+  rows and column aggregation is per block row), so a single SpMV needs
+  no exchange: x is replicated, each rank owns a y slice.
+* ``global_agg`` makes the th0 decision global: every rank computes its
+  shard's block statistics with ``cbspmv_block_stats``, the counts are summed
+  across ranks, and ``cbspmv_decide_agg`` applies the rule; the result is passed
+  as ``agg_mode`` to every shard's ``cbspmv_build``.
+* ``PowerIteration`` is the iterated-SpMV driver of BASELINE config 5:
+  per step y_k = A (x_k / ||y_{k-1}||) (the normalisation folded into the x load
+  by ``cbspmv_spmv_scaled``), then sum(y_k^2) all-reduced and y shards all-gathered
+  into the next x over NCCL.
+
+Collectives go through ``torch.distributed`` (NCCL on GPUs, gloo in CPU tests);
+the compute steps are injected so the host logic is testable without a GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def shard_bounds(row_ptr: np.ndarray, parts: int, blk: int = 16) -> np.ndarray:
+    """Row cut points r_0 = 0 <= r_1 <= ... <= r_P = m at block-row boundaries, balanced by nnz."""
+    m = len(row_ptr) - 1
+    nbr = (m + blk - 1) // blk
+    br_end = np.minimum((np.arange(nbr) + 1) * blk, m)
+    cum = row_ptr[br_end] if nbr else np.zeros(0, np.int64)  # nnz of block rows [0, b]
+    total = int(row_ptr[-1]) if m else 0
+    cuts = [0]
+    for k in range(1, parts):
+        target = total * k / parts
+        b = int(np.searchsorted(cum, target, side="left"))  # first block row with cum >= target
+        r = min(m, (b + 1) * blk) if total else min(m, (m * k // parts) // blk * blk)
+        cuts.append(max(cuts[-1], r))
+    cuts.append(m)
+    return np.asarray(cuts, np.int64)
+
+
+def equal_bounds(m: int, parts: int, blk: int = 16) -> np.ndarray:
+    """Equal row shards rounded to block rows (used when every row has the same nnz)."""
+    cuts = [min(m, (m * k // parts) // blk * blk) for k in range(parts)] + [m]
+    return np.asarray(cuts, np.int64)
+
+
+def slice_rows(A, r0: int, r1: int):
+    """Rows [r0, r1) of a CSR as a CSR with global n (a row shard, P:433 block rows intact)."""
+    from types import SimpleNamespace
+    b, e = int(A.row_ptr[r0]), int(A.row_ptr[r1])
+    return SimpleNamespace(m=r1 - r0, n=A.n, row_ptr=(A.row_ptr[r0:r1 + 1] - b).astype(np.int64),
+                           col=A.col[b:e], val=A.val[b:e], r0=getattr(A, "r0", 0) + r0,
+                           name=f"{getattr(A, 'name', 'A')}[{r0}:{r1}]")
+
+
+def global_agg(A_shard, all_reduce_sum, dtype="f64", **opts) -> int:
+    """The th0 decision on the whole matrix from per-shard statistics."""
+    import paper_2605_18515_b200 as cb
+    nb, ss = cb.block_stats(A_shard, dtype=dtype, **opts)
+    tot = all_reduce_sum(np.array([nb, ss], np.int64))
+    return cb.decide_agg(int(tot[0]), int(tot[1]), **{k: v for k, v in opts.items() if k.startswith("th0")})
+
+
+@dataclass
+class PowerIteration:
+    """y_k = A (x_k / sqrt(sumsq_{k-1})); sumsq_k = allreduce(sum y_k^2); x_{k+1} = allgather(y_k).
+
+    spmv_scaled(x, sumsq, y), sumsq_fn(y, out), all_reduce_sum_(t), all_gather_(out, inp)
+    are injected: the C-ABI calls + NCCL on GPUs, the oracle + gloo in CPU tests.
+    The eigenvalue estimate after step k is lambda_k = sqrt(sumsq_k) (x_k has unit norm)."""
+
+    spmv_scaled: object
+    sumsq_fn: object
+    all_reduce_sum_: object
+    all_gather_: object
+
+    def run(self, x, y, sumsq, steps: int, on_step=None):
+        """x: full vector (replicated), y: this rank's shard, sumsq: 1-element accumulator
+        holding sum(x^2) of the initial x (so step 0 normalises x_0)."""
+        for k in range(steps):
+            self.spmv_scaled(x, sumsq, y)
+            self.sumsq_fn(y, sumsq)
+            self.all_reduce_sum_(sumsq)
+            self.all_gather_(x, y)
+            if on_step is not None:
+                on_step(k, x, y, sumsq)
+        return x, sumsq

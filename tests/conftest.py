@@ -17,5 +17,5 @@ def pytest_configure(config):
 def _built():
     """Build the in-tree native libraries once (CPU-side: nvcc cross-compiles)."""
     import subprocess
-    subprocess.run(["make", "-s", "-C", ROOT, "synth", "oracle"], check=True)
+    subprocess.run(["make", "-s", "-C", ROOT, "synth", "oracle", "lib"], check=True)
     yield

@@ -1,0 +1,61 @@
+"""The C-ABI library loads and exports every symbol include/cbspmv.h declares (CPU only)."""
+import os
+import re
+import subprocess
+
+import paper_2605_18515_b200 as cb
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "cbspmv.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cbspmv_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared()
+    for n in ("cbspmv_build", "cbspmv_spmv", "cbspmv_destroy"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = cb.lib()
+    out = subprocess.run(["nm", "-D", "--defined-only", cb.LIB_PATH], capture_output=True, text=True, check=True)
+    exported = set(re.findall(r"\bT (cbspmv_\w+)", out.stdout))
+    for n in declared():
+        assert n in exported, n
+        assert hasattr(lib, n)
+    assert cb.version() == 1
+
+
+def test_status_strings_and_null_safety():
+    L = cb.lib()
+    assert L.cbspmv_status_string(0) == b"CBSPMV_OK"
+    assert L.cbspmv_status_string(6) == b"CBSPMV_EUNSUPPORTED"
+    assert L.cbspmv_destroy(None) == 0
+    assert L.cbspmv_build(1, 1, 0, None, None, None, 0, None, None, None) == 1  # null out
+
+
+def test_no_oracle_in_product_path():
+    """The product package must not import or link the oracle (independence rule)."""
+    pkg = os.path.join(ROOT, "paper_2605_18515_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "liboracle" not in txt and "oracle_" not in txt, f
+    out = subprocess.run(["ldd", cb.LIB_PATH], capture_output=True, text=True)
+    assert "oracle" not in out.stdout
+
+
+def test_host_only_handle_refuses_device_calls():
+    import numpy as np
+    import synth
+    h = cb.build(synth.fig1(), device=-1)
+    st = cb.lib().cbspmv_spmv(h.raw, 8, 16, None)
+    assert st == 6
+    assert h.info["nb"] == 1
+    cb.destroy(h)
+    np.testing.assert_equal(h._raw, None)

@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Bar (BASELINE.json north_star): per row |y - y_ref| <= 1e-12 * R_i in fp64 and
+<= 1e-5 * R_i in fp32, R_i = sum_j |a_ij x_j| (the oracle runs in fp64 on the
+fp32-rounded A and x for fp32); rows with R_i = 0 must be exactly 0.  In
+exact-integer mode every summation order gives identical bits, so y must equal
+the oracle bitwise.  Full BASELINE sizes are checked on sampled rows plus
+closed forms, in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2605_18515_b200 as cb
+import synth
+from tests.test_oracle import CORPUS
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def _ok():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def gpu_spmv(A, x, dtype="f64", **opts):
+    _ok()
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    h = cb.build(A, dtype=dtype, device=0, **opts)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(DEV, tdt)
+    yd = torch.full((A.m,), float("nan"), dtype=tdt, device=DEV)  # spmv must overwrite every row
+    cb.spmv(h, xd, yd)
+    torch.cuda.synchronize()
+    return yd.cpu().numpy().astype(np.float64), h
+
+
+def check_rows(y, y_ref, R, rel):
+    assert y.shape == y_ref.shape
+    assert np.all(np.isfinite(y))
+    diff = np.abs(y - y_ref)
+    bad = diff > rel * R
+    if bad.any():
+        i = int(np.argmax(bad))
+        raise AssertionError(f"{bad.sum()} rows out of tolerance; row {i}: y={y[i]!r} ref={y_ref[i]!r} R={R[i]!r}")
+
+
+def ref32(A, x):
+    A32 = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
+    return oracle.spmv_csr(A32, x.astype(np.float32).astype(np.float64))
+
+
+# ----------------------------------------------------------------------------- corpus, every variant
+@pytest.mark.parametrize("A", CORPUS, ids=lambda A: A.name)
+def test_corpus_fp64_default(A):
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=5)
+    y_ref, R = oracle.spmv_csr(A, x)
+    y, _ = gpu_spmv(A, x)
+    check_rows(y, y_ref, R, 1e-12)
+
+
+@pytest.mark.parametrize("A", CORPUS[::2], ids=lambda A: A.name)
+@pytest.mark.parametrize("agg", [0, 1])
+@pytest.mark.parametrize("ff", [-1, 0, 1, 2])
+@pytest.mark.parametrize("bal", [0, 1])
+def test_corpus_fp64_variants(A, agg, ff, bal):
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=6)
+    y_ref, R = oracle.spmv_csr(A, x)
+    y, _ = gpu_spmv(A, x, agg_mode=agg, force_format=ff, balance=bal)
+    check_rows(y, y_ref, R, 1e-12)
+
+
+@pytest.mark.parametrize("A", CORPUS[::3], ids=lambda A: A.name)
+@pytest.mark.parametrize("agg", [0, 1])
+@pytest.mark.parametrize("ff", [-1, 0, 1, 2])
+def test_corpus_fp32(A, agg, ff):
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=8)
+    y_ref, R = ref32(A, x)
+    y, _ = gpu_spmv(A, x, dtype="f32", agg_mode=agg, force_format=ff)
+    check_rows(y, y_ref, R, 1e-5)
+
+
+@pytest.mark.parametrize("pattern", ["random", "hub", "blockdense", "banded"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("agg", [0, 1])
+def test_exact_integer_mode_bitwise(pattern, dtype, agg):
+    A = synth.random_csr(300, 260, 0.08, 17, val_mode=2, pattern=pattern)
+    x = synth.vector(A.n, synth.VEC_INT7)
+    y_ref, _ = oracle.spmv_csr(A, x)
+    for ff in (-1, 0, 1, 2):
+        y, _ = gpu_spmv(A, x, dtype=dtype, agg_mode=agg, force_format=ff)
+        assert np.array_equal(y, y_ref)
+
+
+def test_fig1_fixture_all_paths():
+    A = synth.fig1()
+    x = synth.vector(16, synth.VEC_FIG1)
+    y_ref, _ = oracle.spmv_csr(A, x)
+    for ff in (-1, 0, 1, 2):
+        y, h = gpu_spmv(A, x, force_format=ff)
+        assert y.tolist() == y_ref.tolist()
+
+
+# ----------------------------------------------------------------------------- API semantics
+def test_add_scaled_host_and_sumsq():
+    _ok()
+    A = synth.random_csr(500, 400, 0.05, 21, pattern="hub")
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=2)
+    y_ref, R = oracle.spmv_csr(A, x)
+    h = cb.build(A, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    y0 = torch.from_numpy(synth.vector(A.m, synth.VEC_UNIFORM, seed=9)).to(DEV)
+    y = y0.clone()
+    cb.spmv_add(h, xd, y)
+    torch.cuda.synchronize()
+    y0h = y0.cpu().numpy()
+    assert np.all(np.abs((y.cpu().numpy() - y0h) - y_ref) <= 1e-12 * (R + np.abs(y0h)))
+    # scaled: y := A (x / sqrt(ss)) with ss = 4 -> A x / 2 exactly (power-of-two scale)
+    ss = torch.tensor([4.0], dtype=torch.float64, device=DEV)
+    ys = torch.empty(A.m, dtype=torch.float64, device=DEV)
+    cb.spmv_scaled(h, xd, ss, ys)
+    yu = torch.empty_like(ys)
+    cb.spmv(h, xd, yu)
+    torch.cuda.synchronize()
+    check_rows(ys.cpu().numpy() * 2.0, y_ref, R, 1e-12)
+    # host buffers end to end
+    yh = np.empty(A.m, np.float64)
+    cb.spmv_host(h, x, yh)
+    check_rows(yh, y_ref, R, 1e-12)
+    # sumsq
+    out = torch.zeros(1, dtype=torch.float64, device=DEV)
+    cb.sumsq(xd, out)
+    torch.cuda.synchronize()
+    assert abs(out.item() - float(np.dot(x, x))) <= 1e-12 * float(np.dot(x, x))
+
+
+def test_non_default_stream_and_repeat():
+    _ok()
+    A = synth.make("rmat", small=True)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=4)
+    y_ref, R = oracle.spmv_csr(A, x)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        h = cb.build(A, device=0)
+        xd = torch.from_numpy(x).to(DEV)
+        ys = [torch.empty(A.m, dtype=torch.float64, device=DEV) for _ in range(3)]
+        for y in ys:
+            cb.spmv(h, xd, y)
+    s.synchronize()
+    for y in ys:
+        check_rows(y.cpu().numpy(), y_ref, R, 1e-12)
+
+
+def test_degenerate():
+    _ok()
+    for m, n in [(0, 5), (5, 1), (1, 1), (17, 3), (3, 17), (33, 2000)]:
+        A = synth.random_csr(m, n, 0.5, 3) if m else synth.CSR(0, n, np.zeros(1, np.int64), np.zeros(0, np.int32),
+                                                              np.zeros(0))
+        x = synth.vector(n, synth.VEC_UNIFORM, seed=1)
+        y_ref, R = oracle.spmv_csr(A, x)
+        y, _ = gpu_spmv(A, x)
+        check_rows(y, y_ref, R, 1e-12)
+    Z = synth.CSR(40, 40, np.zeros(41, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    y, h = gpu_spmv(Z, np.ones(40))
+    assert np.all(y == 0.0) and h.info["nb"] == 0
+
+
+def test_dense_block_in_partial_last_block_row():
+    """m not a multiple of 16: the dense path must not write rows >= m."""
+    _ok()
+    d = np.zeros((37, 40))
+    d[32:37, 16:32] = np.arange(1, 81).reshape(5, 16)
+    d[0:16, 0:16] = 1.0
+    A = synth.from_dense(d)
+    x = synth.vector(40, synth.VEC_INT7)
+    y_ref, _ = oracle.spmv_csr(A, x)
+    tdt = torch.float64
+    h = cb.build(A, device=0, force_format=2)
+    guard = torch.full((48,), 7.0, dtype=tdt, device=DEV)
+    cb.spmv(h, torch.from_numpy(x).to(DEV), guard[:37])
+    torch.cuda.synchronize()
+    g = guard.cpu().numpy()
+    assert np.array_equal(g[:37], y_ref) and np.all(g[37:] == 7.0)
+
+
+# ----------------------------------------------------------------------------- device layout
+def decode_stream(stream, page_off, info, blk=16):
+    """Decode the device page stream back into per-block (row0, xcol0, nnz, type, ncols, record bytes)."""
+    out = []
+    for p in range(len(page_off) - 1):
+        pg = stream[int(page_off[p]):int(page_off[p + 1])]
+        nblk = int(pg[:4].view(np.uint32)[0])
+        desc = pg[16:16 + 16 * nblk].view(np.uint32).reshape(nblk, 4)
+        for b in range(nblk):
+            row0, xcol0, w2, ncols = (int(v) for v in desc[b])
+            off = (w2 & 0xFFFF) * 16
+            nnz = ((w2 >> 16) & 0xFF) + 1
+            typ = (w2 >> 24) & 3
+            out.append((row0, xcol0, nnz, typ, ncols, pg, off))
+    return out
+
+
+@pytest.mark.parametrize("name", ["laplace", "rmat", "clustered"])
+def test_device_stream_encodes_canonical_format(name):
+    """What is on the device is exactly the canonical format (slot order), records byte-equal."""
+    _ok()
+    A = synth.make(name, small=True)
+    h = cb.build(A, device=0)
+    ex = cb.export(h)
+    s, po = cb.download_stream(h)
+    blocks = decode_stream(s, po, h.info)
+    assert len(blocks) == ex["nb"]
+    S = 8
+    agg = h.info["agg"]
+    for i, (row0, xcol0, nnz, typ, ncols, pg, off) in enumerate(blocks):
+        br, bc = int(ex["blk_row_idx"][i]), int(ex["blk_col_idx"][i])
+        assert row0 == 16 * br and nnz == ex["nnz_per_blk"][i] and typ == ex["type_per_blk"][i]
+        idx = nnz if typ == 0 else (17 + nnz if typ == 1 else 0)
+        size = idx + (-idx) % S + (256 if typ == 2 else nnz) * S
+        vp = int(ex["vp_per_blk"][i])
+        if agg:
+            seg0 = int(ex["cols_offset"][br]) + 16 * bc
+            seg1 = int(ex["cols_offset"][br + 1])
+            assert ncols == min(16, seg1 - seg0)
+            rest = pg[off:off + 4 * ncols].view(np.uint32)
+            assert np.array_equal(rest, ex["restore_cols"][seg0:seg0 + ncols])
+            off += 4 * ((ncols + 3) // 4 * 4)
+        else:
+            assert xcol0 == 16 * bc and ncols == min(16, A.n - 16 * bc)
+        assert np.array_equal(pg[off:off + size], ex["mtx_data"][vp:vp + size])
+
+
+# ----------------------------------------------------------------------------- BASELINE configs
+@pytest.mark.parametrize("name", ["laplace", "rmat", "clustered", "uniform"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_configs_small_full_check(name, dtype):
+    A = synth.make(name, small=True)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=12)
+    y_ref, R = oracle.spmv_csr(A, x) if dtype == "f64" else ref32(A, x)
+    y, h = gpu_spmv(A, x, dtype=dtype)
+    check_rows(y, y_ref, R, 1e-12 if dtype == "f64" else 1e-5)
+
+
+def test_laplace_config2_full():
+    """Config 2 at full size: x = 1 closed form (exact) and random x vs the oracle."""
+    A = synth.laplace5(1000)
+    y, h = gpu_spmv(A, np.ones(A.n))
+    g = 1000
+    gy, gx = np.divmod(np.arange(g * g), g)
+    nb = (gy > 0).astype(int) + (gy < g - 1) + (gx > 0) + (gx < g - 1)
+    assert h.info["agg"] == 1
+    assert np.array_equal(y, 4.0 - nb)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=21)
+    y_ref, R = oracle.spmv_csr(A, x)
+    y, _ = gpu_spmv(A, x)
+    check_rows(y, y_ref, R, 1e-12)
+
+
+def sampled(A, y, x, rel, k=20000, seed=0):
+    rows = np.sort(np.random.default_rng(seed).choice(A.m, size=min(k, A.m), replace=False))
+    rows = np.unique(np.concatenate([rows, [0, 1, 2, A.m - 1]]))  # hub rows of R-MAT are low ids
+    y_ref, R = oracle.spmv_rows(A, x, rows)
+    check_rows(y[rows], y_ref, R, rel)
+
+
+def test_rmat_config3_full_sampled():
+    """Config 3 (bench workload) at full size: sampled rows + the x = 1 row-sum identity."""
+    A = synth.make("rmat")
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=32)
+    y, h = gpu_spmv(A, x)
+    assert h.info["agg"] == 1
+    sampled(A, y, x, 1e-12)
+    y1, _ = gpu_spmv(A, np.ones(A.n))
+    rows = np.repeat(np.arange(A.m), np.diff(A.row_ptr))
+    rs = np.bincount(rows, weights=np.abs(A.val), minlength=A.m)
+    sums = np.bincount(rows, weights=A.val, minlength=A.m)
+    assert np.all(np.abs(y1 - sums) <= 1e-12 * rs)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_clustered_config4_full_sampled(dtype):
+    A = synth.make("clustered")
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=42)
+    y, h = gpu_spmv(A, x, dtype=dtype)
+    assert h.info["agg"] == 0 and min(h.info["fmt_count"]) > 0
+    if dtype == "f64":
+        sampled(A, y, x, 1e-12)
+    else:
+        rows = np.sort(np.random.default_rng(1).choice(A.m, size=20000, replace=False))
+        A32 = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
+        y_ref, R = oracle.spmv_rows(A32, x.astype(np.float32).astype(np.float64), rows)
+        check_rows(y[rows], y_ref, R, 1e-5)
