@@ -35,10 +35,11 @@
 
 namespace {
 
-constexpr int kConsumerWarps = 16;
+constexpr int kConsumerWarps = 24;
 constexpr int kThreads = 32 * (1 + kConsumerWarps);
 constexpr int kMaxStages = 16;
-constexpr int kBatch = 4;  // blocks per consumer warp whose x gathers are issued together
+constexpr int kSmemHeader = 512;  // full[16], empty[16] mbarriers + claim[16] counters; keeps stages aligned
+constexpr int kBatch = 4;         // blocks per claim: x gathers of 2 blocks per load instruction
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -92,70 +93,123 @@ __device__ __forceinline__ void red_add(V *p, V v) {
 
 __device__ __forceinline__ int pad_to(int bytes, int a) { return (bytes + a - 1) & ~(a - 1); }
 
-// ------------------------------------------------------------------ per-format warp paths
-// COO (Alg. 3): lane <-> element, segmented per-row reduction, RED per distinct row.
+struct Blk {          // a decoded 16-byte descriptor
+  uint32_t row0;      // y row base (blk_row_idx * 16)
+  int nnz;            // 1..256; 0 = no block
+  int type;           // CBSPMV_FMT_*; 3 = no block
+  const uint8_t *body;  // the canonical record (after the inlined restore entries)
+};
+
+template <bool AGG>
+__device__ __forceinline__ Blk decode(const uint8_t *page, uint4 d) {
+  Blk b;
+  b.row0 = d.x;
+  b.type = (d.z >> 24) & 3;
+  b.nnz = b.type == 3 ? 0 : (int)((d.z >> 16) & 0xFF) + 1;
+  const uint8_t *rec = page + ((d.z & 0xFFFFu) << 4);
+  b.body = AGG ? rec + ((d.w + 3u) & ~3u) * 4u : rec;
+  return b;
+}
+
+// Segmented warp reduction over rows sorted within [lane, end): after the rounds, each
+// segment head holds its segment's sum.  Rounds adapt to the longest segment.
 template <typename V>
-__device__ __forceinline__ void coo_path(const uint8_t *body, int nnz, uint32_t row0, V xr, V *__restrict__ y,
-                                         int lane) {
-  const V *vals = reinterpret_cast<const V *>(body + pad_to(nnz, (int)sizeof(V)));
-  for (int base = 0; base < nnz; base += 32) {
-    const int e = base + lane;
-    const bool valid = e < nnz;
-    const uint32_t b = valid ? body[e] : 0u;
-    const int row = b & 15, col = b >> 4;
+__device__ __forceinline__ V seg_reduce(V p, bool head, int end, int lane) {
+  const int seglen = head ? end - lane : 0;
+  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)seglen);
+  for (int d = 1; d < maxlen; d <<= 1) {
+    const V o = __shfl_down_sync(kFull, p, d);
+    if (lane + d < end) p += o;
+  }
+  return p;
+}
+
+// ------------------------------------------------------------------ per-format warp paths
+// COO (Alg. 3), one block per warp: lane <-> element (chunks of 32 when forced on dense blocks).
+// xr holds the block's x tile in lanes base..base+15.
+template <typename V>
+__device__ __forceinline__ void coo_path(const Blk &b, V xr, int base, V *__restrict__ y, int lane) {
+  const V *vals = reinterpret_cast<const V *>(b.body + pad_to(b.nnz, (int)sizeof(V)));
+  for (int c0 = 0; c0 < b.nnz; c0 += 32) {
+    const int e = c0 + lane;
+    const bool valid = e < b.nnz;
+    const uint32_t byte = valid ? b.body[e] : 0u;
+    const int row = byte & 15, col = byte >> 4;
     const V v = valid ? vals[e] : V(0);
-    const V xv = __shfl_sync(kFull, xr, col);
+    const V xv = __shfl_sync(kFull, xr, base + col);
     V p = v * xv;
     const int prow = __shfl_up_sync(kFull, row, 1);
     const bool head = valid && (lane == 0 || prow != row);
     const uint32_t heads = __ballot_sync(kFull, head);
-    const int nvalid = min(32, nnz - base);
     const uint32_t above = heads & ~((2u << lane) - 1u);
-    const int end = above ? __ffs(above) - 1 : nvalid;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const V o = __shfl_down_sync(kFull, p, d);
-      if (lane + d < end) p += o;
-    }
-    if (head) red_add(y + row0 + row, p);
+    const int lim = min(32, b.nnz - c0);
+    const int end = above ? min(__ffs(above) - 1, lim) : lim;
+    p = seg_reduce(p, head, end, lane);
+    if (head) red_add(y + b.row0 + row, p);
   }
 }
 
-// CSR: 17 u8 row_ptr, nnz u8 local cols, pad, values; lanes 2r, 2r+1 share row r.
+// Two COO blocks with nnz <= 16 in one warp: lanes 0-15 block A, lanes 16-31 block B;
+// xr holds A's x tile in lanes 0-15 and B's in lanes 16-31.
 template <typename V>
-__device__ __forceinline__ void csr_path(const uint8_t *body, int nnz, uint32_t row0, V xr, V *__restrict__ y,
-                                         int lane) {
-  const uint8_t *cols = body + 17;
-  const V *vals = reinterpret_cast<const V *>(body + pad_to(17 + nnz, (int)sizeof(V)));
+__device__ __forceinline__ void coo_pair_path(const Blk &A, const Blk &B, V xr, V *__restrict__ y, int lane) {
+  const int h = lane >> 4, i = lane & 15;
+  const uint8_t *body = h ? B.body : A.body;
+  const int nnz = h ? B.nnz : A.nnz;
+  const uint32_t row0 = h ? B.row0 : A.row0;
+  const V *vals = reinterpret_cast<const V *>(body + pad_to(nnz, (int)sizeof(V)));
+  const bool valid = i < nnz;
+  const uint32_t byte = valid ? body[i] : 0u;
+  const int row = byte & 15, col = byte >> 4;
+  const V v = valid ? vals[i] : V(0);
+  const V xv = __shfl_sync(kFull, xr, (h << 4) | col);
+  V p = v * xv;
+  const int prow = __shfl_up_sync(kFull, row, 1);
+  const bool head = valid && (i == 0 || prow != row);
+  const uint32_t heads = __ballot_sync(kFull, head);
+  const uint32_t above = heads & ~((2u << lane) - 1u);
+  const int lim = (h << 4) + nnz;
+  const int end = above ? min(__ffs(above) - 1, lim) : lim;
+  p = seg_reduce(p, head, end, lane);
+  if (head) red_add(y + row0 + row, p);
+}
+
+// CSR: 17 u8 row_ptr, nnz u8 local cols, pad, values; lanes 2r, 2r+1 share row r
+// ("32 threads collaboratively compute 16 y elements").
+template <typename V>
+__device__ __forceinline__ void csr_path(const Blk &b, V xr, int base, V *__restrict__ y, int lane) {
+  const uint8_t *cols = b.body + 17;
+  const V *vals = reinterpret_cast<const V *>(b.body + pad_to(17 + b.nnz, (int)sizeof(V)));
   const int r = lane >> 1, h = lane & 1;
-  const int lo = body[r];
-  const int hi = r < 15 ? (int)body[r + 1] : nnz;  // row_ptr[16] = nnz (R-8)
+  const int lo = b.body[r];
+  const int hi = r < 15 ? (int)b.body[r + 1] : b.nnz;  // row_ptr[16] = nnz (R-8)
   const int len = hi - lo;
   const int k = len > h ? (len - h + 1) >> 1 : 0;
-  const int kmax = __reduce_max_sync(kFull, (unsigned)k);
+  const int kmax = (int)__reduce_max_sync(kFull, (unsigned)k);
   V acc = V(0);
   for (int t = 0; t < kmax; t++) {
     const int e = lo + h + 2 * t;
     const bool valid = t < k;
     const int c = valid ? cols[e] : 0;
     const V v = valid ? vals[e] : V(0);
-    const V xv = __shfl_sync(kFull, xr, c);
+    const V xv = __shfl_sync(kFull, xr, base + c);
     if (valid) acc = fma(v, xv, acc);
   }
   acc += __shfl_xor_sync(kFull, acc, 1);
-  if (h == 0 && len > 0) red_add(y + row0 + r, acc);
+  if (h == 0 && len > 0) red_add(y + b.row0 + r, acc);
 }
 
-// DENSE (Alg. 4): element k*32 + lane is (row 2k + lane/16, col lane%16): the lane's own x.
+// DENSE (Alg. 4): element k*32 + lane is (row 2k + lane/16, col lane%16); a transposing
+// xor-butterfly (8, 4, 2, 1) leaves the full sum of row 2*((lane>>1)&7) + lane/16 in lane pairs.
 template <typename V>
-__device__ __forceinline__ void dense_path(const uint8_t *body, uint32_t row0, V xr, V *__restrict__ y, int64_t m,
-                                           int lane) {
-  const V *vals = reinterpret_cast<const V *>(body);
+__device__ __forceinline__ void dense_path(const Blk &b, V xr, int base, V *__restrict__ y, int64_t m, int lane) {
+  const V *vals = reinterpret_cast<const V *>(b.body);
+  const V xl = __shfl_sync(kFull, xr, base + (lane & 15));
   V p[8];
 #pragma unroll
   for (int k = 0; k < 8; k++) {
     const V v = vals[k * 32 + lane];
-    p[k] = v != V(0) ? v * xr : V(0);  // absent entries contribute 0 (explicit zeros were dropped)
+    p[k] = v != V(0) ? v * xl : V(0);  // absent entries contribute 0 (explicit zeros were dropped)
   }
   const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
   V q[4];
@@ -180,7 +234,14 @@ __device__ __forceinline__ void dense_path(const uint8_t *body, uint32_t row0, V
   }
   s += __shfl_xor_sync(kFull, s, 1);
   const int row = 2 * ((lane >> 1) & 7) + (lane >> 4);
-  if ((lane & 1) == 0 && (int64_t)row0 + row < m) red_add(y + row0 + row, s);
+  if ((lane & 1) == 0 && (int64_t)b.row0 + row < m) red_add(y + b.row0 + row, s);
+}
+
+template <typename V>
+__device__ __forceinline__ void single_path(const Blk &b, V xr, int base, V *__restrict__ y, int64_t m, int lane) {
+  if (b.type == CBSPMV_FMT_COO) coo_path<V>(b, xr, base, y, lane);
+  else if (b.type == CBSPMV_FMT_CSR) csr_path<V>(b, xr, base, y, lane);
+  else if (b.type == CBSPMV_FMT_DENSE) dense_path<V>(b, xr, base, y, m, lane);
 }
 
 // ------------------------------------------------------------------ the persistent kernel
@@ -200,7 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + kMaxStages;
-  uint8_t *ring = smem + 2 * kMaxStages * sizeof(uint64_t);  // 256 B: keeps stages 128-B aligned
+  uint32_t *claim = reinterpret_cast<uint32_t *>(empty + kMaxStages);
+  uint8_t *ring = smem + kSmemHeader;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t p0 = P.cta_page[blockIdx.x], p1 = P.cta_page[blockIdx.x + 1];
@@ -210,79 +272,84 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < S; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
+      claim[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (warp == 0) {
-    // ---------------- producer
+    // ---------------- producer: one bulk copy per page into the ring
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      uint32_t i = 0;
-      for (uint32_t p = p0; p < p1; p++, i++) {
-        const int s = i % S;
-        const uint32_t round = i / S;
-        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+      int s = 0;
+      uint32_t round = 0;
+      for (uint32_t p = p0; p < p1; p++) {
+        if (round > 0) {
+          mbar_wait(&empty[s], (round - 1) & 1);  // every consumer warp released the stage
+          claim[s] = 0;                           // published by the release of arrive below
+        }
         const uint64_t off = P.page_off[p];
         const uint32_t bytes = (uint32_t)(P.page_off[p + 1] - off);
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(ring + (size_t)s * P.page_cap, P.stream + off, bytes, &full[s], pol);
+        if (++s == S) { s = 0; round++; }
       }
     }
     return;
   }
 
-  // ---------------- consumers
-  const int cw = warp - 1;
+  // ---------------- consumers: claim kBatch blocks at a time from the current page
   V scale = V(1);
   if constexpr (SCALED) scale = (V)(1.0 / sqrt(*P.sumsq));
-  const int c16 = lane & 15;
-  uint32_t i = 0;
-  for (uint32_t p = p0; p < p1; p++, i++) {
-    const int s = i % S;
-    mbar_wait(&full[s], (i / S) & 1);
+  const int c16 = lane & 15, hl = lane >> 4;
+  int s = 0;
+  uint32_t parity = 0;
+  for (uint32_t p = p0; p < p1; p++) {
+    mbar_wait(&full[s], parity);
     const uint8_t *page = ring + (size_t)s * P.page_cap;
     const int nblk = *reinterpret_cast<const uint32_t *>(page);
-    for (int b0 = cw * kBatch; b0 < nblk; b0 += kConsumerWarps * kBatch) {
-      uint4 d[kBatch];
-      V xr[kBatch];
+    const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
+    for (;;) {
+      uint32_t b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&claim[s], (uint32_t)kBatch);
+      b0 = __shfl_sync(kFull, b0, 0);
+      if ((int)b0 >= nblk) break;
+      const int nb = min(kBatch, nblk - (int)b0);
+      Blk blk[kBatch];
+      V xr[kBatch / 2];
 #pragma unroll
       for (int u = 0; u < kBatch; u++) {
-        const int b = b0 + u;
-        xr[u] = V(0);
-        d[u] = make_uint4(0, 0, 3u << 24, 0);
-        if (b < nblk) {
-          d[u] = *reinterpret_cast<const uint4 *>(page + cb::kPageHeader + cb::kDescBytes * b);
-          if (c16 < (int)d[u].w) {
-            uint32_t col;
-            if constexpr (AGG) {
-              const uint32_t *restore = reinterpret_cast<const uint32_t *>(page + ((d[u].z & 0xFFFFu) << 4));
-              col = restore[c16];
-            } else {
-              col = d[u].y + c16;
-            }
-            xr[u] = __ldg(x + col);
-          }
+        const uint4 d = u < nb ? descs[b0 + u] : make_uint4(0, 0, 3u << 24, 0);
+        blk[u] = decode<AGG>(page, d);
+      }
+      // x tiles: lanes 0-15 gather block 2g, lanes 16-31 block 2g+1
+#pragma unroll
+      for (int g = 0; g < kBatch / 2; g++) {
+        const uint4 d = (2 * g + hl) < nb ? descs[b0 + 2 * g + hl] : make_uint4(0, 0, 3u << 24, 0);
+        xr[g] = V(0);
+        if (c16 < (int)d.w) {
+          uint32_t col;
+          if constexpr (AGG) col = reinterpret_cast<const uint32_t *>(page + ((d.z & 0xFFFFu) << 4))[c16];
+          else col = d.y + c16;
+          xr[g] = __ldg(x + col);
+          if constexpr (SCALED) xr[g] *= scale;
         }
       }
 #pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        const uint32_t w2 = d[u].z;
-        const int type = (w2 >> 24) & 3;
-        if (type == 3) continue;  // warp-uniform
-        const int nnz = (int)((w2 >> 16) & 0xFF) + 1;
-        const uint8_t *rec = page + ((w2 & 0xFFFFu) << 4);
-        const uint8_t *body = AGG ? rec + ((d[u].w + 3u) & ~3u) * 4u : rec;
-        V xv = xr[u];
-        if constexpr (SCALED) xv *= scale;
-        if (type == CBSPMV_FMT_COO) coo_path<V>(body, nnz, d[u].x, xv, y, lane);
-        else if (type == CBSPMV_FMT_CSR) csr_path<V>(body, nnz, d[u].x, xv, y, lane);
-        else dense_path<V>(body, d[u].x, xv, y, P.m, lane);
+      for (int g = 0; g < kBatch / 2; g++) {
+        const Blk &A = blk[2 * g], &B = blk[2 * g + 1];
+        if (A.type == CBSPMV_FMT_COO && A.nnz <= 16 && (B.type == 3 || (B.type == CBSPMV_FMT_COO && B.nnz <= 16))) {
+          coo_pair_path<V>(A, B, xr[g], y, lane);
+        } else {
+          single_path<V>(A, xr[g], 0, y, P.m, lane);
+          single_path<V>(B, xr[g], 16, y, P.m, lane);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == S) { s = 0; parity ^= 1u; }
   }
 }
 
@@ -345,7 +412,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute", err);
-  const int header = 2 * kMaxStages * (int)sizeof(uint64_t);
+  const int header = kSmemHeader;
   int nstage = (optin - header) / dev->page_cap;
   if (nstage > kMaxStages) nstage = kMaxStages;
   if (nstage < 2) {
@@ -380,7 +447,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
   }
   if (dev.n_pages > 0) {
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, dev.page_cap, dev.nstage};
-    const int smem = 2 * kMaxStages * (int)sizeof(uint64_t) + dev.nstage * dev.page_cap;
+    const int smem = kSmemHeader + dev.nstage * dev.page_cap;
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
     cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(kThreads), args, (size_t)smem, st);
