@@ -422,26 +422,48 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
   parallel_for(c.nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
     for (int64_t i = lo; i < hi; i++) { int nc; rec[i] = dev_record_bytes(c, i, canon_record_bytes(c, i), &nc); ncol[i] = nc; }
   });
-  // Greedy pages of whole thread blocks (slot order), each <= page_cap bytes.
+  // Work items of a block range: COO groups (consecutive COO blocks, nnz sum <= 32) and
+  // single CSR / DENSE blocks.  Returns the number of items.
+  auto count_items = [&](int64_t b0, int64_t b1) {
+    int64_t items = 0, lanes = 32;
+    for (int64_t i = b0; i < b1; i++) {
+      if (c.type[i] == CBSPMV_FMT_COO && c.nnzb[i] <= 32) {
+        if (lanes + c.nnzb[i] > 32) { items++; lanes = 0; }
+        lanes += c.nnzb[i];
+      } else {
+        items++; lanes = 32;
+      }
+    }
+    return items;
+  };
+  auto page_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
+    return kPageHeader + kDescBytes * (b1 - b0) + round_up(2 * count_items(b0, b1), 16) + rec_bytes;
+  };
+  const int64_t tile = 16 * (int64_t)c.val_size;  // x tile bytes per block (device-gathered)
+  auto stage_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
+    return round_up(page_bytes(b0, b1, rec_bytes), 16) + tile * (b1 - b0);
+  };
+  // Greedy pages of whole thread blocks (slot order): page + x tiles <= stage capacity.
   std::vector<int64_t> page_tb;  // first TB of each page
   std::vector<uint64_t> off;
-  int64_t total = 0, cur = -1;
-  int64_t cur_bytes = 0;
+  int64_t total = 0;
+  int64_t cur_tb = -1, cur_rec = 0;
   for (int64_t t = 0; t < c.T; t++) {
-    int64_t tb_bytes = 0;
-    for (int64_t i = c.tb_ptr[t]; i < c.tb_ptr[t + 1]; i++) tb_bytes += kDescBytes + rec[i];
-    if (kPageHeader + tb_bytes > page_cap) {
-      *err = "page capacity too small for one thread block";
-      return CBSPMV_EINVAL;
+    int64_t tb_rec = 0;
+    for (int64_t i = c.tb_ptr[t]; i < c.tb_ptr[t + 1]; i++) tb_rec += rec[i];
+    if (page_cap > kMaxPageCap || stage_bytes(c.tb_ptr[t], c.tb_ptr[t + 1], tb_rec) > page_cap) {
+      *err = "stage capacity too small for one thread block";
+      return CBSPMV_EUNSUPPORTED;
     }
-    if (cur < 0 || cur_bytes + tb_bytes > page_cap) {
-      if (cur >= 0) total += round_up(cur_bytes, 16);
+    bool fits = cur_tb >= 0 && stage_bytes(c.tb_ptr[cur_tb], c.tb_ptr[t + 1], cur_rec + tb_rec) <= page_cap;
+    if (!fits) {
+      if (cur_tb >= 0) total += round_up(page_bytes(c.tb_ptr[cur_tb], c.tb_ptr[t], cur_rec), 16);
       page_tb.push_back(t); off.push_back((uint64_t)total);
-      cur = t; cur_bytes = kPageHeader;
+      cur_tb = t; cur_rec = 0;
     }
-    cur_bytes += tb_bytes;
+    cur_rec += tb_rec;
   }
-  if (cur >= 0) total += round_up(cur_bytes, 16);
+  if (cur_tb >= 0) total += round_up(page_bytes(c.tb_ptr[cur_tb], c.tb_ptr[c.T], cur_rec), 16);
   off.push_back((uint64_t)total);
   page_tb.push_back(c.T);
   const int64_t npages = (int64_t)off.size() - 1;
@@ -456,28 +478,63 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
     s->bytes = (uint8_t *)p;
   }
   parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
+    std::vector<uint32_t> w;
+    std::vector<uint16_t> items;
     for (int64_t p = lo; p < hi; p++) {
       uint8_t *page = s->bytes + off[p];
-      int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
-      int64_t nblk = b1 - b0;
+      const int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
+      const int64_t nblk = b1 - b0;
+      w.assign((size_t)nblk, 0);
       std::memset(page, 0, (size_t)(off[p + 1] - off[p]));
-      uint32_t hdr[4] = {(uint32_t)nblk, (uint32_t)page_tb[p], (uint32_t)(page_tb[p + 1] - page_tb[p]), 0};
-      std::memcpy(page, hdr, 16);
-      int64_t pos = kPageHeader + kDescBytes * nblk;  // already a multiple of 16
+      // work items
+      items.clear();
+      int64_t lanes = 32, head = -1;
       for (int64_t i = b0; i < b1; i++) {
+        const int64_t k = c.nnzb[i];
+        if (c.type[i] == CBSPMV_FMT_COO && k <= 32) {
+          if (lanes + k > 32) { head = i; items.push_back((uint16_t)(i - b0)); lanes = 0; }
+          w[i - b0] = (uint32_t)lanes << 25;         // first lane of the block in its group
+          lanes += k;
+        } else {
+          head = i; items.push_back((uint16_t)(i - b0)); lanes = 32;
+          w[i - b0] = 0;
+        }
+        (void)head;
+      }
+      const int64_t nitems = (int64_t)items.size();
+      const int64_t item_off = kPageHeader + kDescBytes * nblk;
+      const int64_t x_off = (int64_t)(off[p + 1] - off[p]);  // x tiles follow the page in its stage
+      uint32_t hdr[4] = {(uint32_t)nblk, (uint32_t)nitems, (uint32_t)item_off, (uint32_t)x_off};
+      std::memcpy(page, hdr, 16);
+      std::memcpy(page + item_off, items.data(), (size_t)nitems * 2);
+      // group sizes on the heads
+      std::vector<uint32_t> gsize(nblk, 1);
+      for (int64_t it = 0; it < nitems; it++) {
+        const int64_t hb = items[it], he = it + 1 < nitems ? items[it + 1] : nblk;
+        gsize[hb] = (uint32_t)(he - hb);
+      }
+      int64_t pos = item_off + round_up(2 * nitems, 16);
+      int64_t next_item = 0;
+      for (int64_t i = b0; i < b1; i++) {
+        const int64_t k = c.nnzb[i], S = c.val_size;
+        const int type = c.type[i];
+        const bool is_head = next_item < nitems && items[next_item] == i - b0;
+        if (is_head) next_item++;
+        const int64_t idx = type == CBSPMV_FMT_COO ? k : type == CBSPMV_FMT_CSR ? (c.blk + 1) + k : 0;
+        const int64_t body = pos + (c.agg ? round_up(ncol[i], 4) * 4 : 0);
+        const int64_t vals = body + round_up(idx, S);
         Desc d;
         d.row0 = (uint32_t)c.br[i] * (uint32_t)c.blk;
-        d.xcol0 = c.agg ? 0u : (uint32_t)c.bc[i] * (uint32_t)c.blk;
-        d.w2 = pack_w2((uint32_t)(pos / 16), (uint32_t)c.nnzb[i], c.type[i]);
-        d.ncols = (uint32_t)ncol[i];
+        d.xinfo = c.agg ? (uint32_t)pos : (uint32_t)c.bc[i] * (uint32_t)c.blk;
+        d.offs = (uint32_t)body | ((uint32_t)vals << 16);
+        d.w = pack_w((uint32_t)k, (uint32_t)type, (uint32_t)ncol[i], is_head, is_head ? gsize[i - b0] : 1u, 0u) |
+              w[i - b0];
         std::memcpy(page + kPageHeader + kDescBytes * (i - b0), &d, sizeof(d));
-        uint8_t *r = page + pos;
         if (c.agg) {
           const uint32_t *seg = c.restore.data() + c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk;
-          std::memcpy(r, seg, (size_t)ncol[i] * 4);
-          r += round_up(ncol[i], 4) * 4;
+          std::memcpy(page + pos, seg, (size_t)ncol[i] * 4);
         }
-        std::memcpy(r, c.mtx.data() + c.vp[i], (size_t)canon_record_bytes(c, i));
+        std::memcpy(page + body, c.mtx.data() + c.vp[i], (size_t)canon_record_bytes(c, i));
         pos += rec[i];
       }
     }

@@ -153,7 +153,7 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
     DeviceGuard g(h->device);
     cb::Stream S;
     const char *env = std::getenv("CBSPMV_PAGE_BYTES");
-    int cap = env ? std::atoi(env) : cb::kDefaultPageCap;
+    int cap = env ? std::atoi(env) : cb::kDefaultStageCap;
     cap = (int)cb::round_up(std::max(cap, 1024), 16);
     st = cb::build_stream(c, cap, o.host_threads, &S, &err);
     if (st != CBSPMV_OK) { cb::free_stream(&S); delete h; return fail(st, err); }

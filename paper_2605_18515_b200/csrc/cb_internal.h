@@ -13,25 +13,35 @@ namespace cb {
 // ---------------------------------------------------------------------------
 // Device page stream.  A derived layout of the canonical
 // format: blocks in slot order (after Alg. 2), whole thread blocks per page,
-// each page = header | desc[nblk] | records, every record 16-byte aligned and
-// prefixed by its block row's restore_cols entries when aggregated.
-// One cp.async.bulk moves a whole page into shared memory.
+//   page = header | desc[nblk] | item[nitems] (u16) | records
+// every record 16-byte aligned and preceded by its block's restore_cols entries
+// when aggregated.  One cp.async.bulk moves a whole page into a
+// shared-memory stage; the page's x tiles (16 values per block, gathered on the
+// device) follow it in the same stage, so pages are sized by
+// bytes + 16 * size(Val) * nblk <= stage capacity.  Work items: a COO group
+// (consecutive COO blocks whose nnz sum to <= 32, one warp, one lane per element)
+// or a single CSR / DENSE block.
 // ---------------------------------------------------------------------------
-constexpr int kPageHeader = 16;     // u32 nblk, u32 first_tb, u32 tb_count, u32 reserved
-constexpr int kDescBytes = 16;      // see Desc
-constexpr int kDefaultPageCap = 17408;  // >= 16 + 8*16 + 8*(64 + 2048): one fp64 TB of 8 dense blocks
-constexpr int kMaxPageCap = 65536 * 16 - 16;  // record offsets are u16 in 16-byte units
+constexpr int kPageHeader = 16;         // u32 nblk, u32 nitems, u32 item_off, u32 x_off (x tiles in the stage)
+constexpr int kDescBytes = 16;          // see Desc
+constexpr int kDefaultStageCap = 28672; // 8 stages in 227 KB; >= one fp64 TB of 8 dense blocks + tiles
+constexpr int kMaxPageCap = 65536;      // descriptor offsets are u16 bytes
 
-// 16-byte block descriptor, read with one 128-bit shared load.
+// 16-byte block descriptor, read with one 128-bit shared load.  All offsets are bytes from
+// the page start, precomputed on the host so the kernel does no record parsing.
 struct Desc {
-  uint32_t row0;    // blk_row_idx * 16
-  uint32_t xcol0;   // blk_col_idx * 16 without aggregation, 0 with it
-  uint32_t w2;      // [0,16) record offset / 16 from page start; [16,24) nnz - 1; [24,26) type
-  uint32_t ncols;   // valid x-tile columns (restore entries when aggregated), 0..16
+  uint32_t row0;    // blk_row_idx * 16: y row base
+  uint32_t xinfo;   // without aggregation: blk_col_idx * 16 (x tile base);
+                    // with aggregation: page offset of the block's restore_cols entries
+  uint32_t offs;    // [0,16) page offset of the canonical record; [16,32) page offset of its values
+  uint32_t w;       // [0,8) nnz - 1; [8,10) type; [11,16) group size - 1 (on a group head);
+                    // [16,21) ncols (valid x-tile columns, 0..16); [24] group head;
+                    // [25,30) first lane of the block within its COO group
 };
+constexpr uint32_t kFlagHead = 1u << 24;
 
-inline uint32_t pack_w2(uint32_t rec_off16, uint32_t nnz, uint32_t type) {
-  return rec_off16 | ((nnz - 1u) << 16) | (type << 24);
+inline uint32_t pack_w(uint32_t nnz, uint32_t type, uint32_t ncols, bool head, uint32_t gsize, uint32_t lane0) {
+  return (nnz - 1u) | (type << 8) | ((gsize - 1u) << 11) | (ncols << 16) | (head ? kFlagHead : 0u) | (lane0 << 25);
 }
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }

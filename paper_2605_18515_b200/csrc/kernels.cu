@@ -29,17 +29,20 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "cb_internal.h"
 
 namespace {
 
-constexpr int kConsumerWarps = 24;
-constexpr int kThreads = 32 * (1 + kConsumerWarps);
+constexpr int kGatherWarps = 4;
+constexpr int kGroups = 4;                    // consumer warp groups; page i goes to group i % kGroups
+constexpr int kGroupWarps = 6;                // warps per group (share one page, claim its items)
+constexpr int kConsumerWarps = kGroups * kGroupWarps;
+constexpr int kThreads = 32 * (1 + kGatherWarps + kConsumerWarps);
 constexpr int kMaxStages = 16;
-constexpr int kSmemHeader = 512;  // full[16], empty[16] mbarriers + claim[16] counters; keeps stages aligned
-constexpr int kBatch = 4;         // blocks per claim: x gathers of 2 blocks per load instruction
+constexpr int kSmemHeader = 640;  // full / xready / empty mbarriers [16] + claim counters [16]
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -85,126 +88,111 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
       : "memory");
 }
+// Asynchronous gather of one x value into shared memory (SASS LDGSTS).
+template <typename V>
+__device__ __forceinline__ void cp_async_elem(V *dst, const V *src) {
+  // no "memory" clobber: the destination is read only after the xready mbarrier wait
+  if constexpr (sizeof(V) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src));
+}
+// Arrive on an mbarrier once all of this thread's prior cp.async copies have landed.
+__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Ablation knob for profiling only (env CBSPMV_DEBUG_SKIP, a kernel argument held in a
+// register): bit 0 drops the y atomics, bit 1 replaces the x gathers.  0 in production.
+struct Dbg {
+  int skip;
+};
 
 template <typename V>
-__device__ __forceinline__ void red_add(V *p, V v) {
+__device__ __forceinline__ void red_add(V *p, V v, Dbg dbg) {
+  if (dbg.skip & 1) {
+    if (v == V(12345.678)) *p = v;  // keep the value live without the atomic
+    return;
+  }
   atomicAdd(p, v);  // result unused -> RED.E.ADD
 }
 
-__device__ __forceinline__ int pad_to(int bytes, int a) { return (bytes + a - 1) & ~(a - 1); }
-
-struct Blk {          // a decoded 16-byte descriptor
-  uint32_t row0;      // y row base (blk_row_idx * 16)
-  int nnz;            // 1..256; 0 = no block
-  int type;           // CBSPMV_FMT_*; 3 = no block
-  const uint8_t *body;  // the canonical record (after the inlined restore entries)
-};
-
-template <bool AGG>
-__device__ __forceinline__ Blk decode(const uint8_t *page, uint4 d) {
-  Blk b;
-  b.row0 = d.x;
-  b.type = (d.z >> 24) & 3;
-  b.nnz = b.type == 3 ? 0 : (int)((d.z >> 16) & 0xFF) + 1;
-  const uint8_t *rec = page + ((d.z & 0xFFFFu) << 4);
-  b.body = AGG ? rec + ((d.w + 3u) & ~3u) * 4u : rec;
-  return b;
-}
-
-// Segmented warp reduction over rows sorted within [lane, end): after the rounds, each
-// segment head holds its segment's sum.  Rounds adapt to the longest segment.
-template <typename V>
-__device__ __forceinline__ V seg_reduce(V p, bool head, int end, int lane) {
-  const int seglen = head ? end - lane : 0;
-  const int maxlen = (int)__reduce_max_sync(kFull, (unsigned)seglen);
-  for (int d = 1; d < maxlen; d <<= 1) {
-    const V o = __shfl_down_sync(kFull, p, d);
-    if (lane + d < end) p += o;
-  }
-  return p;
-}
+__device__ __forceinline__ int d_type(const uint4 &d) { return (d.w >> 8) & 3; }
+__device__ __forceinline__ int d_nnz(const uint4 &d) { return (int)(d.w & 0xFF) + 1; }
+__device__ __forceinline__ int d_ncols(const uint4 &d) { return (d.w >> 16) & 31; }
+__device__ __forceinline__ int d_gsize(const uint4 &d) { return (int)((d.w >> 11) & 31) + 1; }
+__device__ __forceinline__ int d_lane0(const uint4 &d) { return (int)((d.w >> 25) & 31); }
 
 // ------------------------------------------------------------------ per-format warp paths
-// COO (Alg. 3), one block per warp: lane <-> element (chunks of 32 when forced on dense blocks).
-// xr holds the block's x tile in lanes base..base+15.
-template <typename V>
-__device__ __forceinline__ void coo_path(const Blk &b, V xr, int base, V *__restrict__ y, int lane) {
-  const V *vals = reinterpret_cast<const V *>(b.body + pad_to(b.nnz, (int)sizeof(V)));
-  for (int c0 = 0; c0 < b.nnz; c0 += 32) {
-    const int e = c0 + lane;
-    const bool valid = e < b.nnz;
-    const uint32_t byte = valid ? b.body[e] : 0u;
-    const int row = byte & 15, col = byte >> 4;
-    const V v = valid ? vals[e] : V(0);
-    const V xv = __shfl_sync(kFull, xr, base + col);
-    V p = v * xv;
-    const int prow = __shfl_up_sync(kFull, row, 1);
-    const bool head = valid && (lane == 0 || prow != row);
-    const uint32_t heads = __ballot_sync(kFull, head);
-    const uint32_t above = heads & ~((2u << lane) - 1u);
-    const int lim = min(32, b.nnz - c0);
-    const int end = above ? min(__ffs(above) - 1, lim) : lim;
-    p = seg_reduce(p, head, end, lane);
-    if (head) red_add(y + b.row0 + row, p);
+// xt: the block's 16-value x tile in shared memory (filled by the gather warps):
+//   x[bc*16 + c] without aggregation (the paper's shared-memory s_x), or
+//   x[restore_cols[cols_offset[br] + bc*16 + c]] with aggregation.
+
+// COO group (Alg. 3): consecutive COO blocks packed into one warp, lane <-> element; the
+// coordinate byte gives row = b & 15, col = b >> 4; one RED per element into y,
+// Alg. 3's atomicAdd, issued as one warp instruction.
+template <typename V, bool SCALED>
+__device__ __forceinline__ void coo_group(const uint8_t *page, const uint4 *descs, int hb, int gsize,
+                                          const V *xbuf, V scale, V *__restrict__ y, int lane, Dbg dbg) {
+  const uint4 dj = descs[hb + min(lane, gsize - 1)];
+  const uint32_t starts = __reduce_or_sync(kFull, lane < gsize ? 1u << d_lane0(dj) : 0u);
+  const int mi = __popc(starts & ((2u << lane) - 1u)) - 1;  // member block of this lane
+  const uint4 d = descs[hb + mi];
+  const int i = lane - d_lane0(d);
+  const bool valid = i < d_nnz(d);
+  const uint8_t *body = page + (d.z & 0xFFFFu);
+  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const uint32_t byte = valid ? body[i] : 0u;
+  const int row = byte & 15, col = byte >> 4;
+  if (valid) {
+    V p = vals[i] * xbuf[(hb + mi) * 16 + col];
+    if constexpr (SCALED) p *= scale;
+    red_add(y + d.x + row, p, dbg);
   }
 }
 
-// Two COO blocks with nnz <= 16 in one warp: lanes 0-15 block A, lanes 16-31 block B;
-// xr holds A's x tile in lanes 0-15 and B's in lanes 16-31.
-template <typename V>
-__device__ __forceinline__ void coo_pair_path(const Blk &A, const Blk &B, V xr, V *__restrict__ y, int lane) {
-  const int h = lane >> 4, i = lane & 15;
-  const uint8_t *body = h ? B.body : A.body;
-  const int nnz = h ? B.nnz : A.nnz;
-  const uint32_t row0 = h ? B.row0 : A.row0;
-  const V *vals = reinterpret_cast<const V *>(body + pad_to(nnz, (int)sizeof(V)));
-  const bool valid = i < nnz;
-  const uint32_t byte = valid ? body[i] : 0u;
-  const int row = byte & 15, col = byte >> 4;
-  const V v = valid ? vals[i] : V(0);
-  const V xv = __shfl_sync(kFull, xr, (h << 4) | col);
-  V p = v * xv;
-  const int prow = __shfl_up_sync(kFull, row, 1);
-  const bool head = valid && (i == 0 || prow != row);
-  const uint32_t heads = __ballot_sync(kFull, head);
-  const uint32_t above = heads & ~((2u << lane) - 1u);
-  const int lim = (h << 4) + nnz;
-  const int end = above ? min(__ffs(above) - 1, lim) : lim;
-  p = seg_reduce(p, head, end, lane);
-  if (head) red_add(y + row0 + row, p);
+// A COO block too large for a group (forced format): chunks of 32 elements.
+template <typename V, bool SCALED>
+__device__ __forceinline__ void coo_big(const uint8_t *page, const uint4 &d, const V *xt, V scale,
+                                        V *__restrict__ y, int lane, Dbg dbg) {
+  const uint8_t *body = page + (d.z & 0xFFFFu);
+  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const int nnz = d_nnz(d);
+  for (int e = lane; e < nnz; e += 32) {
+    const uint32_t byte = body[e];
+    V p = vals[e] * xt[byte >> 4];
+    if constexpr (SCALED) p *= scale;
+    red_add(y + d.x + (byte & 15), p, dbg);
+  }
 }
 
 // CSR: 17 u8 row_ptr, nnz u8 local cols, pad, values; lanes 2r, 2r+1 share row r
 // ("32 threads collaboratively compute 16 y elements").
-template <typename V>
-__device__ __forceinline__ void csr_path(const Blk &b, V xr, int base, V *__restrict__ y, int lane) {
-  const uint8_t *cols = b.body + 17;
-  const V *vals = reinterpret_cast<const V *>(b.body + pad_to(17 + b.nnz, (int)sizeof(V)));
+template <typename V, bool SCALED>
+__device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, const V *xt, V scale,
+                                         V *__restrict__ y, int lane, Dbg dbg) {
+  const uint8_t *body = page + (d.z & 0xFFFFu);
+  const uint8_t *cols = body + 17;
+  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const int nnz = d_nnz(d);
   const int r = lane >> 1, h = lane & 1;
-  const int lo = b.body[r];
-  const int hi = r < 15 ? (int)b.body[r + 1] : b.nnz;  // row_ptr[16] = nnz (R-8)
-  const int len = hi - lo;
-  const int k = len > h ? (len - h + 1) >> 1 : 0;
-  const int kmax = (int)__reduce_max_sync(kFull, (unsigned)k);
+  const int lo = body[r];
+  const int hi = r < 15 ? (int)body[r + 1] : nnz;  // row_ptr[16] = nnz (R-8)
   V acc = V(0);
-  for (int t = 0; t < kmax; t++) {
-    const int e = lo + h + 2 * t;
-    const bool valid = t < k;
-    const int c = valid ? cols[e] : 0;
-    const V v = valid ? vals[e] : V(0);
-    const V xv = __shfl_sync(kFull, xr, base + c);
-    if (valid) acc = fma(v, xv, acc);
-  }
+  for (int e = lo + h; e < hi; e += 2) acc = fma(vals[e], xt[cols[e]], acc);
   acc += __shfl_xor_sync(kFull, acc, 1);
-  if (h == 0 && len > 0) red_add(y + b.row0 + r, acc);
+  if constexpr (SCALED) acc *= scale;
+  if (h == 0 && hi > lo) red_add(y + d.x + r, acc, dbg);
 }
 
 // DENSE (Alg. 4): element k*32 + lane is (row 2k + lane/16, col lane%16); a transposing
 // xor-butterfly (8, 4, 2, 1) leaves the full sum of row 2*((lane>>1)&7) + lane/16 in lane pairs.
-template <typename V>
-__device__ __forceinline__ void dense_path(const Blk &b, V xr, int base, V *__restrict__ y, int64_t m, int lane) {
-  const V *vals = reinterpret_cast<const V *>(b.body);
-  const V xl = __shfl_sync(kFull, xr, base + (lane & 15));
+template <typename V, bool SCALED>
+__device__ __forceinline__ void dense_path(const uint8_t *page, const uint4 &d, const V *xt, V scale,
+                                           V *__restrict__ y, int64_t m, int lane, Dbg dbg) {
+  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  V xl = (lane & 15) < d_ncols(d) ? xt[lane & 15] : V(0);
+  if constexpr (SCALED) xl *= scale;
   V p[8];
 #pragma unroll
   for (int k = 0; k < 8; k++) {
@@ -234,14 +222,7 @@ __device__ __forceinline__ void dense_path(const Blk &b, V xr, int base, V *__re
   }
   s += __shfl_xor_sync(kFull, s, 1);
   const int row = 2 * ((lane >> 1) & 7) + (lane >> 4);
-  if ((lane & 1) == 0 && (int64_t)b.row0 + row < m) red_add(y + b.row0 + row, s);
-}
-
-template <typename V>
-__device__ __forceinline__ void single_path(const Blk &b, V xr, int base, V *__restrict__ y, int64_t m, int lane) {
-  if (b.type == CBSPMV_FMT_COO) coo_path<V>(b, xr, base, y, lane);
-  else if (b.type == CBSPMV_FMT_CSR) csr_path<V>(b, xr, base, y, lane);
-  else if (b.type == CBSPMV_FMT_DENSE) dense_path<V>(b, xr, base, y, m, lane);
+  if ((lane & 1) == 0 && (int64_t)d.x + row < m) red_add(y + d.x + row, s, dbg);
 }
 
 // ------------------------------------------------------------------ the persistent kernel
@@ -251,27 +232,32 @@ struct KParams {
   const uint32_t *cta_page;
   int64_t m;
   const double *sumsq;
-  int page_cap;
+  int stage;     // bytes per stage: page data + its x tiles
   int nstage;
+  Dbg dbg;
 };
 
+// Warp roles: 0 = TMA producer, 1..kGatherWarps = x gatherers, the rest = consumers.
 template <typename V, bool AGG, bool SCALED>
 __global__ void __launch_bounds__(kThreads, 1)
     cb_spmv_kernel(KParams P, const V *__restrict__ x, V *__restrict__ y) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-  uint64_t *empty = full + kMaxStages;
+  uint64_t *xready = full + kMaxStages;
+  uint64_t *empty = xready + kMaxStages;
   uint32_t *claim = reinterpret_cast<uint32_t *>(empty + kMaxStages);
   uint8_t *ring = smem + kSmemHeader;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t p0 = P.cta_page[blockIdx.x], p1 = P.cta_page[blockIdx.x + 1];
   const int S = P.nstage;
+  const Dbg dbg = P.dbg;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&xready[s], 32 * kGatherWarps);
+      mbar_init(&empty[s], kGroupWarps);
       claim[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -292,64 +278,94 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t off = P.page_off[p];
         const uint32_t bytes = (uint32_t)(P.page_off[p + 1] - off);
         mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(ring + (size_t)s * P.page_cap, P.stream + off, bytes, &full[s], pol);
+        bulk_g2s(ring + (size_t)s * P.stage, P.stream + off, bytes, &full[s], pol);
         if (++s == S) { s = 0; round++; }
       }
     }
     return;
   }
 
-  // ---------------- consumers: claim kBatch blocks at a time from the current page
+  if (warp <= kGatherWarps) {
+    // ---------------- gatherers: x tile of every block of the page -> shared (cp.async)
+    const int gt = (warp - 1) * 32 + lane;
+    int s = 0;
+    uint32_t parity = 0;
+    for (uint32_t p = p0; p < p1; p++) {
+      mbar_wait(&full[s], parity);
+      const uint8_t *page = ring + (size_t)s * P.stage;
+      const int nblk = *reinterpret_cast<const uint32_t *>(page);
+      V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + reinterpret_cast<const uint32_t *>(page)[3]);
+      const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
+      constexpr int kG = 32 * kGatherWarps, kU = 4;
+      const int lim = nblk * 16;
+      for (int t0 = gt; t0 < lim; t0 += kG * kU) {
+        uint32_t col[kU];
+        bool ok[kU];
+#pragma unroll
+        for (int j = 0; j < kU; j++) {  // independent: descriptor + restore loads of kU tiles first
+          const int t = t0 + j * kG;
+          ok[j] = false;
+          col[j] = 0;
+          if (t < lim) {
+            const uint4 d = descs[t >> 4];
+            const int c = t & 15;
+            ok[j] = c < d_ncols(d);
+            if (ok[j]) col[j] = AGG ? reinterpret_cast<const uint32_t *>(page + d.y)[c] : d.y + c;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kU; j++) {
+          if (ok[j]) {
+            V *dst = xbuf + t0 + j * kG;
+            if (dbg.skip & 2) *dst = V(1) + V(col[j] & 1);
+            else cp_async_elem(dst, x + col[j]);
+          }
+        }
+      }
+      cp_async_arrive(&xready[s]);
+      if (++s == S) { s = 0; parity ^= 1u; }
+    }
+    return;
+  }
+
+  // ---------------- consumers: group g takes pages g, g + kGroups, ...; its warps claim the
+  // page's work items one at a time
   V scale = V(1);
   if constexpr (SCALED) scale = (V)(1.0 / sqrt(*P.sumsq));
-  const int c16 = lane & 15, hl = lane >> 4;
-  int s = 0;
-  uint32_t parity = 0;
-  for (uint32_t p = p0; p < p1; p++) {
+  const int cw = warp - 1 - kGatherWarps;
+  const int grp = cw / kGroupWarps;
+  int s = grp % S;
+  uint32_t parity = (uint32_t)((grp / S) & 1);
+  for (uint32_t p = p0 + grp; p < p1; p += kGroups) {
     mbar_wait(&full[s], parity);
-    const uint8_t *page = ring + (size_t)s * P.page_cap;
-    const int nblk = *reinterpret_cast<const uint32_t *>(page);
+    mbar_wait(&xready[s], parity);
+    const uint8_t *page = ring + (size_t)s * P.stage;
+    const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
+    const int nitems = (int)hdr[1];
+    const uint16_t *items = reinterpret_cast<const uint16_t *>(page + hdr[2]);
+    const V *xbuf = reinterpret_cast<const V *>(page + hdr[3]);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
     for (;;) {
-      uint32_t b0 = 0;
-      if (lane == 0) b0 = atomicAdd(&claim[s], (uint32_t)kBatch);
-      b0 = __shfl_sync(kFull, b0, 0);
-      if ((int)b0 >= nblk) break;
-      const int nb = min(kBatch, nblk - (int)b0);
-      Blk blk[kBatch];
-      V xr[kBatch / 2];
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        const uint4 d = u < nb ? descs[b0 + u] : make_uint4(0, 0, 3u << 24, 0);
-        blk[u] = decode<AGG>(page, d);
-      }
-      // x tiles: lanes 0-15 gather block 2g, lanes 16-31 block 2g+1
-#pragma unroll
-      for (int g = 0; g < kBatch / 2; g++) {
-        const uint4 d = (2 * g + hl) < nb ? descs[b0 + 2 * g + hl] : make_uint4(0, 0, 3u << 24, 0);
-        xr[g] = V(0);
-        if (c16 < (int)d.w) {
-          uint32_t col;
-          if constexpr (AGG) col = reinterpret_cast<const uint32_t *>(page + ((d.z & 0xFFFFu) << 4))[c16];
-          else col = d.y + c16;
-          xr[g] = __ldg(x + col);
-          if constexpr (SCALED) xr[g] *= scale;
-        }
-      }
-#pragma unroll
-      for (int g = 0; g < kBatch / 2; g++) {
-        const Blk &A = blk[2 * g], &B = blk[2 * g + 1];
-        if (A.type == CBSPMV_FMT_COO && A.nnz <= 16 && (B.type == 3 || (B.type == CBSPMV_FMT_COO && B.nnz <= 16))) {
-          coo_pair_path<V>(A, B, xr[g], y, lane);
-        } else {
-          single_path<V>(A, xr[g], 0, y, P.m, lane);
-          single_path<V>(B, xr[g], 16, y, P.m, lane);
-        }
+      uint32_t k = 0;
+      if (lane == 0) k = atomicAdd(&claim[s], 1u);
+      k = __shfl_sync(kFull, k, 0);
+      if ((int)k >= nitems) break;
+      const int hb = items[k];
+      const uint4 dh = descs[hb];
+      const int t = d_type(dh);
+      if (t == CBSPMV_FMT_COO) {
+        if (d_nnz(dh) <= 32) coo_group<V, SCALED>(page, descs, hb, d_gsize(dh), xbuf, scale, y, lane, dbg);
+        else coo_big<V, SCALED>(page, dh, xbuf + hb * 16, scale, y, lane, dbg);
+      } else if (t == CBSPMV_FMT_CSR) {
+        csr_path<V, SCALED>(page, dh, xbuf + hb * 16, scale, y, lane, dbg);
+      } else {
+        dense_path<V, SCALED>(page, dh, xbuf + hb * 16, scale, y, P.m, lane, dbg);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (++s == S) { s = 0; parity ^= 1u; }
+    s += kGroups;
+    if (s >= S) { s -= S; parity ^= 1u; }
   }
 }
 
@@ -413,19 +429,19 @@ int cb_configure(CbDevice *dev, std::string *err) {
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute", err);
   const int header = kSmemHeader;
-  int nstage = (optin - header) / dev->page_cap;
+  const int stage = dev->page_cap;
+  int nstage = (optin - header) / stage;
   if (nstage > kMaxStages) nstage = kMaxStages;
-  if (nstage < 2) {
+  if (nstage < kGroups + 1) {
     *err = "page capacity too large for shared memory";
     return CBSPMV_EUNSUPPORTED;
   }
   dev->nstage = nstage;
   dev->consumers = kConsumerWarps;
-  const int smem = header + nstage * dev->page_cap;
   for (int dt = 0; dt < 2; dt++)
     for (int agg = 0; agg < 2; agg++)
       for (int sc = 0; sc < 2; sc++) {
-        e = cudaFuncSetAttribute(select_kernel(dt, agg, sc), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = cudaFuncSetAttribute(select_kernel(dt, agg, sc), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
       }
   const int sms = sm_count(dev->device);
@@ -445,9 +461,14 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     if (dev.dtype == CBSPMV_F64) cb_zero_kernel<double><<<zg, zb, 0, st>>>((double *)y, dev.m);
     else cb_zero_kernel<float><<<zg, zb, 0, st>>>((float *)y, dev.m);
   }
+  static const int dbg_skip = [] {
+    const char *v = std::getenv("CBSPMV_DEBUG_SKIP");
+    return v ? std::atoi(v) : 0;
+  }();
   if (dev.n_pages > 0) {
-    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, dev.page_cap, dev.nstage};
-    const int smem = kSmemHeader + dev.nstage * dev.page_cap;
+    const int stage = dev.page_cap;
+    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, Dbg{dbg_skip}};
+    const int smem = kSmemHeader + dev.nstage * stage;
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
     cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(kThreads), args, (size_t)smem, st);

@@ -186,19 +186,18 @@ def test_dense_block_in_partial_last_block_row():
 
 
 # ----------------------------------------------------------------------------- device layout
-def decode_stream(stream, page_off, info, blk=16):
-    """Decode the device page stream back into per-block (row0, xcol0, nnz, type, ncols, record bytes)."""
+def decode_stream(stream, page_off):
+    """Decode the device page stream into per-block descriptor fields + page bytes."""
     out = []
     for p in range(len(page_off) - 1):
         pg = stream[int(page_off[p]):int(page_off[p + 1])]
         nblk = int(pg[:4].view(np.uint32)[0])
         desc = pg[16:16 + 16 * nblk].view(np.uint32).reshape(nblk, 4)
         for b in range(nblk):
-            row0, xcol0, w2, ncols = (int(v) for v in desc[b])
-            off = (w2 & 0xFFFF) * 16
-            nnz = ((w2 >> 16) & 0xFF) + 1
-            typ = (w2 >> 24) & 3
-            out.append((row0, xcol0, nnz, typ, ncols, pg, off))
+            row0, xinfo, offs, w = (int(v) for v in desc[b])
+            out.append(dict(row0=row0, xinfo=xinfo, body=offs & 0xFFFF, vals=offs >> 16, nnz=(w & 0xFF) + 1,
+                            type=(w >> 8) & 3, gsize=((w >> 11) & 31) + 1, ncols=(w >> 16) & 31,
+                            head=(w >> 24) & 1, lane0=(w >> 25) & 31, page=pg, slot=b, nblk=nblk))
     return out
 
 
@@ -210,26 +209,49 @@ def test_device_stream_encodes_canonical_format(name):
     h = cb.build(A, device=0)
     ex = cb.export(h)
     s, po = cb.download_stream(h)
-    blocks = decode_stream(s, po, h.info)
+    blocks = decode_stream(s, po)
     assert len(blocks) == ex["nb"]
     S = 8
     agg = h.info["agg"]
-    for i, (row0, xcol0, nnz, typ, ncols, pg, off) in enumerate(blocks):
+    for i, b in enumerate(blocks):
         br, bc = int(ex["blk_row_idx"][i]), int(ex["blk_col_idx"][i])
-        assert row0 == 16 * br and nnz == ex["nnz_per_blk"][i] and typ == ex["type_per_blk"][i]
+        nnz, typ, pg = b["nnz"], b["type"], b["page"]
+        assert b["row0"] == 16 * br and nnz == ex["nnz_per_blk"][i] and typ == ex["type_per_blk"][i]
+        # work items: COO groups of consecutive COO blocks (nnz sum <= 32), others single
+        if typ == 0 and nnz <= 32:
+            assert b["lane0"] + nnz <= 32
+            if b["head"]:
+                assert b["lane0"] == 0
+            else:
+                prev = blocks[i - 1]
+                assert prev["type"] == 0 and b["lane0"] == prev["lane0"] + prev["nnz"]
+        else:
+            assert b["head"] and b["gsize"] == 1 and b["lane0"] == 0
         idx = nnz if typ == 0 else (17 + nnz if typ == 1 else 0)
+        assert b["vals"] == b["body"] + idx + (-idx) % S
         size = idx + (-idx) % S + (256 if typ == 2 else nnz) * S
         vp = int(ex["vp_per_blk"][i])
         if agg:
             seg0 = int(ex["cols_offset"][br]) + 16 * bc
             seg1 = int(ex["cols_offset"][br + 1])
-            assert ncols == min(16, seg1 - seg0)
-            rest = pg[off:off + 4 * ncols].view(np.uint32)
-            assert np.array_equal(rest, ex["restore_cols"][seg0:seg0 + ncols])
-            off += 4 * ((ncols + 3) // 4 * 4)
+            assert b["ncols"] == min(16, seg1 - seg0)
+            rest = pg[b["xinfo"]:b["xinfo"] + 4 * b["ncols"]].view(np.uint32)
+            assert np.array_equal(rest, ex["restore_cols"][seg0:seg0 + b["ncols"]])
         else:
-            assert xcol0 == 16 * bc and ncols == min(16, A.n - 16 * bc)
-        assert np.array_equal(pg[off:off + size], ex["mtx_data"][vp:vp + size])
+            assert b["xinfo"] == 16 * bc and b["ncols"] == min(16, A.n - 16 * bc)
+        assert np.array_equal(pg[b["body"]:b["body"] + size], ex["mtx_data"][vp:vp + size])
+
+
+@pytest.mark.parametrize("segred", ["0", "1"])
+def test_coo_reduction_modes(segred, monkeypatch):
+    """Both COO accumulation modes (RED per element / segmented reduction) match the oracle."""
+    monkeypatch.setenv("CBSPMV_COO_SEGRED", segred)
+    for A in (synth.make("rmat", small=True), synth.random_csr(300, 300, 0.05, 3, pattern="hub")):
+        x = synth.vector(A.n, synth.VEC_UNIFORM, seed=2)
+        y_ref, R = oracle.spmv_csr(A, x)
+        for ff in (-1, 0):
+            y, _ = gpu_spmv(A, x, force_format=ff)
+            check_rows(y, y_ref, R, 1e-12)
 
 
 # ----------------------------------------------------------------------------- BASELINE configs
