@@ -439,7 +439,9 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
   auto page_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
     return kPageHeader + kDescBytes * (b1 - b0) + round_up(2 * count_items(b0, b1), 16) + rec_bytes;
   };
-  const int64_t tile = 16 * (int64_t)c.val_size;  // x tile bytes per block (device-gathered)
+  // x tile bytes per block gathered into the stage (non-aggregated matrices only; with aggregation
+  // the consumer lanes gather x per element)
+  const int64_t tile = c.agg ? 0 : 16 * (int64_t)c.val_size;
   auto stage_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
     return round_up(page_bytes(b0, b1, rec_bytes), 16) + tile * (b1 - b0);
   };

@@ -24,7 +24,7 @@ namespace cb {
 // ---------------------------------------------------------------------------
 constexpr int kPageHeader = 16;         // u32 nblk, u32 nitems, u32 item_off, u32 x_off (x tiles in the stage)
 constexpr int kDescBytes = 16;          // see Desc
-constexpr int kDefaultStageCap = 28672; // 8 stages in 227 KB; >= one fp64 TB of 8 dense blocks + tiles
+constexpr int kDefaultStageCap = 28672;     // 8 stages in one CTA/SM; >= one fp64 TB of 8 dense blocks + tiles
 constexpr int kMaxPageCap = 65536;      // descriptor offsets are u16 bytes
 
 // 16-byte block descriptor, read with one 128-bit shared load.  All offsets are bytes from
@@ -106,6 +106,7 @@ struct CbDevice {
   int page_cap = 0;
   int grid = 0;
   int nstage = 0;
+  int groups = 1;
   int consumers = 0;
   const uint8_t *d_stream = nullptr;
   const uint64_t *d_page_off = nullptr;

@@ -29,6 +29,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -37,12 +38,11 @@
 namespace {
 
 constexpr int kGatherWarps = 4;
-constexpr int kGroups = 4;                    // consumer warp groups; page i goes to group i % kGroups
-constexpr int kGroupWarps = 6;                // warps per group (share one page, claim its items)
-constexpr int kConsumerWarps = kGroups * kGroupWarps;
-constexpr int kThreads = 32 * (1 + kGatherWarps + kConsumerWarps);
+constexpr int kGroupWarps = 6;     // consumer warps per group; a page is consumed by one group
+constexpr int kMaxGroups = 4;      // consumer groups per CTA (runtime: KParams::groups)
+constexpr int kMaxThreads = 32 * (1 + kGatherWarps + kMaxGroups * kGroupWarps);
 constexpr int kMaxStages = 16;
-constexpr int kSmemHeader = 640;  // full / xready / empty mbarriers [16] + claim counters [16]
+constexpr int kSmemHeader = 512;  // mbarriers [3][16] + claims [16]; per-warp x scratch follows the ring
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -88,6 +88,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_nohint(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_tx_complete_local(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
 // Asynchronous gather of one x value into shared memory (SASS LDGSTS).
 template <typename V>
 __device__ __forceinline__ void cp_async_elem(V *dst, const V *src) {
@@ -103,7 +112,8 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
 }
 
 // Ablation knob for profiling only (env CBSPMV_DEBUG_SKIP, a kernel argument held in a
-// register): bit 0 drops the y atomics, bit 1 replaces the x gathers.  0 in production.
+// register): bit 0 drops the y atomics, bit 1 replaces the x gathers, bit 2 skips the item
+// processing, bit 3 skips the gather loop.  0 in production.
 struct Dbg {
   int skip;
 };
@@ -131,9 +141,10 @@ __device__ __forceinline__ int d_lane0(const uint4 &d) { return (int)((d.w >> 25
 // COO group (Alg. 3): consecutive COO blocks packed into one warp, lane <-> element; the
 // coordinate byte gives row = b & 15, col = b >> 4; one RED per element into y,
 // Alg. 3's atomicAdd, issued as one warp instruction.
-template <typename V, bool SCALED>
+template <typename V, bool AGG, bool SCALED>
 __device__ __forceinline__ void coo_group(const uint8_t *page, const uint4 *descs, int hb, int gsize,
-                                          const V *xbuf, V scale, V *__restrict__ y, int lane, Dbg dbg) {
+                                          const V *xbuf, const V *__restrict__ x, V scale, V *__restrict__ y,
+                                          int lane, Dbg dbg) {
   const uint4 dj = descs[hb + min(lane, gsize - 1)];
   const uint32_t starts = __reduce_or_sync(kFull, lane < gsize ? 1u << d_lane0(dj) : 0u);
   const int mi = __popc(starts & ((2u << lane) - 1u)) - 1;  // member block of this lane
@@ -145,10 +156,80 @@ __device__ __forceinline__ void coo_group(const uint8_t *page, const uint4 *desc
   const uint32_t byte = valid ? body[i] : 0u;
   const int row = byte & 15, col = byte >> 4;
   if (valid) {
-    V p = vals[i] * xbuf[(hb + mi) * 16 + col];
+    V xv;
+    if constexpr (AGG) {  // x[restore_cols[cols_offset[br] + bc*16 + col]], straight to a register
+      const uint32_t c = reinterpret_cast<const uint32_t *>(page + d.y)[col];
+      xv = (dbg.skip & 2) ? V(1) + V(c & 1) : __ldg(x + c);
+    } else {
+      xv = xbuf[(hb + mi) * 16 + col];
+    }
+    V p = vals[i] * xv;
     if constexpr (SCALED) p *= scale;
     red_add(y + d.x + row, p, dbg);
   }
+}
+
+// Split-phase COO group for software pipelining: issue() performs every load (descriptors,
+// element, and the x gather) and finish() multiplies and issues the RED, so a warp keeps the x
+// gathers of two work items in flight.
+template <typename V>
+struct CooPend {
+  V v, xv;
+  uint32_t yrow;
+  bool valid;
+};
+
+template <typename V, bool AGG>
+__device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4 *descs, int hb, int gsize,
+                                                const V *xbuf, const V *__restrict__ x, int lane, Dbg dbg) {
+  CooPend<V> r;
+  const uint4 dj = descs[hb + min(lane, gsize - 1)];
+  const uint32_t starts = __reduce_or_sync(kFull, lane < gsize ? 1u << d_lane0(dj) : 0u);
+  const int mi = __popc(starts & ((2u << lane) - 1u)) - 1;
+  const uint4 d = descs[hb + mi];
+  const int i = lane - d_lane0(d);
+  r.valid = i < d_nnz(d);
+  const uint8_t *body = page + (d.z & 0xFFFFu);
+  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const uint32_t byte = r.valid ? body[i] : 0u;
+  const int col = byte >> 4;
+  r.yrow = d.x + (byte & 15);
+  r.v = r.valid ? vals[i] : V(0);
+  r.xv = V(0);
+  if (r.valid) {
+    if constexpr (AGG) {
+      const uint32_t c = reinterpret_cast<const uint32_t *>(page + d.y)[col];
+      r.xv = (dbg.skip & 2) ? V(1) + V(c & 1) : __ldg(x + c);
+    } else {
+      r.xv = xbuf[(hb + mi) * 16 + col];
+    }
+  }
+  return r;
+}
+
+template <typename V, bool SCALED>
+__device__ __forceinline__ void coo_finish(const CooPend<V> &r, V scale, V *__restrict__ y, Dbg dbg) {
+  if (r.valid) {
+    V p = r.v * r.xv;
+    if constexpr (SCALED) p *= scale;
+    red_add(y + r.yrow, p, dbg);
+  }
+}
+
+// x tile of one block loaded by the warp itself (aggregated matrices have no gather warps):
+// lanes 0-15 fetch restore_cols[c] -> x, lanes 16-31 mirror; returned in shared scratch xt.
+template <typename V, bool AGG>
+__device__ __forceinline__ const V *warp_tile(const uint8_t *page, const uint4 &d, const V *__restrict__ x, V *scratch,
+                                              int lane, Dbg dbg) {
+  if constexpr (AGG) {
+    const int c = lane & 15;
+    if (lane < 16 && c < d_ncols(d)) {
+      const uint32_t col = reinterpret_cast<const uint32_t *>(page + d.y)[c];
+      scratch[c] = (dbg.skip & 2) ? V(1) + V(col & 1) : __ldg(x + col);
+    }
+    __syncwarp();
+  }
+  return scratch;
 }
 
 // A COO block too large for a group (forced format): chunks of 32 elements.
@@ -234,12 +315,14 @@ struct KParams {
   const double *sumsq;
   int stage;     // bytes per stage: page data + its x tiles
   int nstage;
+  int groups;    // consumer groups in this CTA (page i of the CTA -> group i % groups)
+  int tile_bulk; // non-aggregated x tiles: one cp.async.bulk per tile (x 16-byte aligned)
   Dbg dbg;
 };
 
 // Warp roles: 0 = TMA producer, 1..kGatherWarps = x gatherers, the rest = consumers.
 template <typename V, bool AGG, bool SCALED>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kMaxThreads, 1)
     cb_spmv_kernel(KParams P, const V *__restrict__ x, V *__restrict__ y) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -247,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *empty = xready + kMaxStages;
   uint32_t *claim = reinterpret_cast<uint32_t *>(empty + kMaxStages);
   uint8_t *ring = smem + kSmemHeader;
+  V *scratch = reinterpret_cast<V *>(ring + (size_t)P.nstage * P.stage);  // 16 values per consumer warp
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t p0 = P.cta_page[blockIdx.x], p1 = P.cta_page[blockIdx.x + 1];
@@ -256,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&xready[s], 32 * kGatherWarps);
+      mbar_init(&xready[s], P.tile_bulk ? 2 : 32 * kGatherWarps);
       mbar_init(&empty[s], kGroupWarps);
       claim[s] = 0;
     }
@@ -286,10 +370,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   if (warp <= kGatherWarps) {
-    // ---------------- gatherers: x tile of every block of the page -> shared (cp.async)
+    if constexpr (AGG) return;  // aggregated matrices: consumers gather x per element
+    // ---------------- gatherers: x tile of every block of the page -> shared
     const int gt = (warp - 1) * 32 + lane;
     int s = 0;
     uint32_t parity = 0;
+    if (P.tile_bulk) {
+      // non-aggregated: tile = x[bc*16 .. bc*16 + ncols) is contiguous -> one TMA bulk copy per
+      // block (16-byte multiple), the odd tail (if any) by a plain load; gather warp 0 only.
+      if (warp != 1) return;
+      for (uint32_t p = p0; p < p1; p++) {
+        mbar_wait(&full[s], parity);
+        const uint8_t *page = ring + (size_t)s * P.stage;
+        const int nblk = *reinterpret_cast<const uint32_t *>(page);
+        V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + reinterpret_cast<const uint32_t *>(page)[3]);
+        const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
+        constexpr int kPer16 = 16 / (int)sizeof(V);  // values per 16 bytes
+        uint32_t bytes = 0;
+        for (int b = lane; b < nblk; b += 32) bytes += (uint32_t)(d_ncols(descs[b]) / kPer16 * 16);
+        bytes = __reduce_add_sync(kFull, bytes);
+        if (lane == 0) mbar_arrive_expect_tx(&xready[s], bytes);
+        __syncwarp();
+        for (int b = lane; b < nblk; b += 32) {
+          const uint4 d = descs[b];
+          const int nc = d_ncols(d), nbulk = nc / kPer16 * kPer16;
+          if (nbulk > 0) {
+            if (dbg.skip & 2) { for (int c = 0; c < nbulk; c++) xbuf[b * 16 + c] = V(1); mbar_tx_complete_local(&xready[s], nbulk * sizeof(V)); }
+            else bulk_g2s_nohint(xbuf + b * 16, x + d.y, (uint32_t)(nbulk * sizeof(V)), &xready[s]);
+          }
+          for (int c = nbulk; c < nc; c++) xbuf[b * 16 + c] = __ldg(x + d.y + c);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xready[s]);
+        if (++s == S) { s = 0; parity ^= 1u; }
+      }
+      return;
+    }
     for (uint32_t p = p0; p < p1; p++) {
       mbar_wait(&full[s], parity);
       const uint8_t *page = ring + (size_t)s * P.stage;
@@ -297,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + reinterpret_cast<const uint32_t *>(page)[3]);
       const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
       constexpr int kG = 32 * kGatherWarps, kU = 4;
-      const int lim = nblk * 16;
+      const int lim = (dbg.skip & 8) ? 0 : nblk * 16;
       for (int t0 = gt; t0 < lim; t0 += kG * kU) {
         uint32_t col[kU];
         bool ok[kU];
@@ -328,44 +444,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
 
-  // ---------------- consumers: group g takes pages g, g + kGroups, ...; its warps claim the
-  // page's work items one at a time
+  // ---------------- consumers: claim the page's work items one at a time (the next claim is
+  // issued before the current item is processed, hiding its latency)
   V scale = V(1);
   if constexpr (SCALED) scale = (V)(1.0 / sqrt(*P.sumsq));
   const int cw = warp - 1 - kGatherWarps;
-  const int grp = cw / kGroupWarps;
+  V *wscratch = scratch + cw * 16;
+  const int G = P.groups, grp = cw / kGroupWarps;
   int s = grp % S;
   uint32_t parity = (uint32_t)((grp / S) & 1);
-  for (uint32_t p = p0 + grp; p < p1; p += kGroups) {
+  for (uint32_t p = p0 + grp; p < p1; p += G) {
     mbar_wait(&full[s], parity);
-    mbar_wait(&xready[s], parity);
+    if constexpr (!AGG) mbar_wait(&xready[s], parity);
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
-    const int nitems = (int)hdr[1];
+    const int nitems = (dbg.skip & 4) ? 0 : (int)hdr[1];
     const uint16_t *items = reinterpret_cast<const uint16_t *>(page + hdr[2]);
     const V *xbuf = reinterpret_cast<const V *>(page + hdr[3]);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
-    for (;;) {
-      uint32_t k = 0;
-      if (lane == 0) k = atomicAdd(&claim[s], 1u);
-      k = __shfl_sync(kFull, k, 0);
-      if ((int)k >= nitems) break;
+    // item pipeline: the COO group claimed last is issued (loads in flight) while the
+    // previous one is finished; other items run synchronously
+    CooPend<V> pend;
+    pend.valid = false;
+    bool have = false;
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(&claim[s], 1u);
+    k = __shfl_sync(kFull, k, 0);
+    while ((int)k < nitems) {
+      uint32_t kn = 0;
+      if (lane == 0) kn = atomicAdd(&claim[s], 1u);
       const int hb = items[k];
       const uint4 dh = descs[hb];
       const int t = d_type(dh);
-      if (t == CBSPMV_FMT_COO) {
-        if (d_nnz(dh) <= 32) coo_group<V, SCALED>(page, descs, hb, d_gsize(dh), xbuf, scale, y, lane, dbg);
-        else coo_big<V, SCALED>(page, dh, xbuf + hb * 16, scale, y, lane, dbg);
-      } else if (t == CBSPMV_FMT_CSR) {
-        csr_path<V, SCALED>(page, dh, xbuf + hb * 16, scale, y, lane, dbg);
+      if (t == CBSPMV_FMT_COO && d_nnz(dh) <= 32) {
+        const CooPend<V> nxt = coo_issue<V, AGG>(page, descs, hb, d_gsize(dh), xbuf, x, lane, dbg);
+        if (have) coo_finish<V, SCALED>(pend, scale, y, dbg);
+        pend = nxt;
+        have = true;
       } else {
-        dense_path<V, SCALED>(page, dh, xbuf + hb * 16, scale, y, P.m, lane, dbg);
+        const V *xt = AGG ? warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg) : xbuf + hb * 16;
+        if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+        else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+        else dense_path<V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
+        __syncwarp();
       }
+      k = __shfl_sync(kFull, kn, 0);
     }
+    if (have) coo_finish<V, SCALED>(pend, scale, y, dbg);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    s += kGroups;
-    if (s >= S) { s -= S; parity ^= 1u; }
+    s += G;
+    while (s >= S) { s -= S; parity ^= 1u; }
   }
 }
 
@@ -428,23 +557,35 @@ int cb_configure(CbDevice *dev, std::string *err) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute", err);
-  const int header = kSmemHeader;
+  int smem_sm = 0;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev->device);
+  // Launch shape (measured on B200): one persistent CTA per SM with 4 consumer
+  // groups of 6 warps sharing an 8-stage ring; CTAs-per-SM / groups are overridable for tuning.
+  const char *env = std::getenv("CBSPMV_CTAS_PER_SM");
+  int ctas = env ? std::atoi(env) : 1;
+  if (ctas < 1) ctas = 1;
+  const char *genv = std::getenv("CBSPMV_GROUPS");
+  int groups = genv ? std::atoi(genv) : 4;
+  groups = std::max(1, std::min(kMaxGroups, groups));
+  dev->groups = groups;
+  const int header = kSmemHeader + groups * kGroupWarps * 16 * (dev->dtype == CBSPMV_F64 ? 8 : 4);
   const int stage = dev->page_cap;
-  int nstage = (optin - header) / stage;
+  const int budget = std::min(optin, smem_sm / ctas - 1024);  // 1 KB per CTA is reserved by the system
+  int nstage = (budget - header) / stage;
   if (nstage > kMaxStages) nstage = kMaxStages;
-  if (nstage < kGroups + 1) {
+  if (nstage < groups + 1) {
     *err = "page capacity too large for shared memory";
     return CBSPMV_EUNSUPPORTED;
   }
   dev->nstage = nstage;
-  dev->consumers = kConsumerWarps;
+  dev->consumers = groups * kGroupWarps;
   for (int dt = 0; dt < 2; dt++)
     for (int agg = 0; agg < 2; agg++)
       for (int sc = 0; sc < 2; sc++) {
         e = cudaFuncSetAttribute(select_kernel(dt, agg, sc), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
       }
-  const int sms = sm_count(dev->device);
+  const int sms = sm_count(dev->device) * ctas;
   int64_t g = dev->n_pages < sms ? dev->n_pages : sms;
   dev->grid = (int)(g < 1 ? 1 : g);
   return CBSPMV_OK;
@@ -467,11 +608,17 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
   }();
   if (dev.n_pages > 0) {
     const int stage = dev.page_cap;
-    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, Dbg{dbg_skip}};
-    const int smem = kSmemHeader + dev.nstage * stage;
+    // TMA-bulk x tiles measured slower than LDGSTS on B200 (the small tile copies queue behind the
+    // page copies in the TMA engine); kept behind CBSPMV_TILE_BULK=1 for experiments.
+    static const int bulk_env = [] { const char *v = std::getenv("CBSPMV_TILE_BULK"); return v ? std::atoi(v) : 0; }();
+    const int tile_bulk = bulk_env && !dev.agg && ((uintptr_t)x % 16 == 0);
+    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, dev.groups, tile_bulk,
+              Dbg{dbg_skip}};
+    const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * (dev.dtype == CBSPMV_F64 ? 8 : 4);
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
-    cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(kThreads), args, (size_t)smem, st);
+    const int threads = 32 * (1 + kGatherWarps + dev.groups * kGroupWarps);
+    cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(threads), args, (size_t)smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "spmv kernel launch", err);
   }
   cudaError_t e = cudaGetLastError();

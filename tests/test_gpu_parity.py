@@ -314,3 +314,21 @@ def test_clustered_config4_full_sampled(dtype):
         A32 = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
         y_ref, R = oracle.spmv_rows(A32, x.astype(np.float32).astype(np.float64), rows)
         check_rows(y[rows], y_ref, R, 1e-5)
+
+
+@pytest.mark.parametrize("name", ["clustered", "rmat"])
+def test_x_not_16_byte_aligned(name):
+    """x only 8-byte aligned: the tile gather falls back from TMA bulk copies to LDGSTS."""
+    _ok()
+    A = synth.make(name, small=True)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=5)
+    y_ref, R = oracle.spmv_csr(A, x)
+    h = cb.build(A, device=0)
+    buf = torch.zeros(A.n + 1, dtype=torch.float64, device=DEV)
+    buf[1:] = torch.from_numpy(x).to(DEV)
+    xs = buf[1:]
+    assert xs.data_ptr() % 16 == 8
+    y = torch.empty(A.m, dtype=torch.float64, device=DEV)
+    cb.spmv(h, xs, y)
+    torch.cuda.synchronize()
+    check_rows(y.cpu().numpy(), y_ref, R, 1e-12)
