@@ -4,6 +4,12 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat|clustered|laplace|uniform]
                     [--dtype f64|f32] [--impl cb|reference]
 
+Default workload: BASELINE configs[3] (block-clustered, 2^22 rows, ~407M nnz,
+fp64) — the large synthetic matrix whose HBM roofline the metric asks for and
+the one config exercising all three warp paths (DESIGN.md §6 explains the
+choice); R-MAT (configs[2]) and the Laplacian (configs[1]) are measured with the
+same protocol in the same run and reported under "config.also".
+
 A step is one y := A·x over the whole (row-sharded) matrix through the C ABI
 (cbspmv_spmv: zero y + the persistent SpMV kernel).  Inputs already resident in
 HBM; the matrix stream (>= 2 GB on the default workload) is far larger than the
@@ -268,6 +274,11 @@ def run_cb(args, rank: int, world: int, local_rank: int):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(A, x_host, args.dtype)
+    also = {}
+    if world == 1 and args.also:
+        names = [n for n in args.also.split(",") if n and n != args.config and n != "uniform"]
+        cb.destroy(h)
+        also = measure_also(names, args.dtype, args.steps, max(args.warmup, 3), local_rank)
 
     if rank == 0:
         line = {
@@ -285,7 +296,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
                 "achieved_hbm_gbs_step": info["alg_bytes"] / (ms * 1e-3) / 1e9,
                 "tb_load_sd": info["tb_load_sd"], "tb_load_sd_natural": info["tb_load_sd_natural"],
                 "gen_s": gen_s, "build_s": info["build_seconds"], "upload_s": info["upload_seconds"],
-                "grid": info["grid"],
+                "grid": info["grid"], "also": also,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "cb_spmv_kernel",
@@ -300,9 +311,53 @@ def run_cb(args, rank: int, world: int, local_rank: int):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    cb.destroy(h)
     if world > 1:
+        cb.destroy(h)
         tdist.destroy_process_group()
+
+
+def measure_also(names, dtype, steps, warmup, local_rank):
+    """Other BASELINE workloads, same protocol (K back-to-back steps, CUDA events), N=1 only."""
+    import torch
+
+    import paper_2605_18515_b200 as cb
+    import synth
+    out = {}
+    dev = torch.device("cuda", local_rank)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    for name in names:
+        A = synth.make(name)
+        h = cb.build(A, dtype=dtype, device=local_rank, keep_host=0)
+        x = torch.from_numpy(synth.vector(A.n, synth.VEC_UNIFORM, seed=7)).to(dev, tdt)
+        y = torch.empty(A.m, dtype=tdt, device=dev)
+        for _ in range(warmup):
+            cb.spmv(h, x, y)
+        st = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(steps):
+            cb.spmv(h, x, y)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(st)
+        for _ in range(steps):
+            cb.spmv_add(h, x, y)
+        k1.record(st)
+        torch.cuda.synchronize()
+        kms = k0.elapsed_time(k1) / steps
+        peak, _ = peaks()
+        i = h.info
+        out[name] = {"workload": WORKLOAD[name], "nnz": int(i["nnz"]), "agg": int(i["agg"]),
+                     "gflops": 2.0 * i["nnz"] / (ms * 1e-3) / 1e9, "ms_per_step": ms, "kernel_ms": kms,
+                     "alg_bytes": int(i["alg_bytes"]),
+                     "hbm_frac": i["alg_bytes"] / (kms * 1e-3) / 1e9 / peak,
+                     "l2_resident": i["alg_bytes"] < 126e6}
+        cb.destroy(h)
+        del A
+    return out
 
 
 def cpu_baseline(A, x, dtype):
@@ -339,7 +394,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="rmat", choices=list(WORKLOAD))
+    ap.add_argument("--config", default="clustered", choices=list(WORKLOAD))
+    ap.add_argument("--also", default="rmat,laplace",
+                    help="other BASELINE workloads timed the same way on N=1 (comma list, '' for none)")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="cb", choices=["cb", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

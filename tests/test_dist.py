@@ -1,0 +1,159 @@
+"""Multi-GPU host logic on CPU: row sharding, the global th0 decision and the power-iteration
+driver, with world_size 2 over torch.distributed gloo.
+
+The per-rank SpMV is the oracle here (a CPU stand-in for the device); the sharded
+builds are the real C-ABI builder in host-only mode.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import paper_2605_18515_b200 as cb
+import synth
+from paper_2605_18515_b200 import dist as cbd
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_bounds_properties():
+    for name in ("rmat", "clustered", "laplace"):
+        A = synth.make(name, small=True)
+        for P in (1, 2, 3, 8):
+            cuts = cbd.shard_bounds(A.row_ptr, P)
+            assert cuts[0] == 0 and cuts[-1] == A.m and len(cuts) == P + 1
+            assert np.all(np.diff(cuts) >= 0)
+            assert all(c % 16 == 0 or c == A.m for c in cuts)
+            loads = np.diff(A.row_ptr[cuts])
+            max_br = max(int(A.row_ptr[min(A.m, r + 16)] - A.row_ptr[r]) for r in range(0, A.m, 16))
+            assert loads.max() - A.nnz / P <= max_br  # within one block row of the ideal share
+    assert cbd.equal_bounds(1 << 15, 8).tolist() == [i * 4096 for i in range(9)]
+
+
+def _worker(rank, world, port, name, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.make(name, small=True)
+        cuts = cbd.shard_bounds(A.row_ptr, world)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        S = cbd.slice_rows(A, r0, r1)
+
+        def allreduce(a):
+            t = torch.from_numpy(np.asarray(a, np.int64).copy())
+            dist.all_reduce(t)
+            return t.numpy()
+
+        agg = cbd.global_agg(S, allreduce)
+        h = cb.build(S, device=-1, agg_mode=agg)
+        ex = cb.export(h)
+        ref = oracle.build(S, agg_mode=agg)
+        same = all(np.array_equal(ex[k], getattr(ref, k)) for k in
+                   ("blk_row_idx", "blk_col_idx", "nnz_per_blk", "type_per_blk", "vp_per_blk", "mtx_data",
+                    "restore_cols", "cols_offset", "tb_ptr", "tb_load"))
+        x = synth.vector(A.n, synth.VEC_UNIFORM, seed=3)
+        y_shard, _ = oracle.spmv_csr(S, x)
+        parts = [None] * world
+        dist.all_gather_object(parts, (r0, y_shard))
+        q.put((rank, agg, same, parts if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["rmat", "clustered"])
+def test_two_rank_sharded_build_and_spmv(name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = synth.make(name, small=True)
+    full = oracle.build(A)
+    for rank, agg, same, _ in res:
+        assert agg == full.agg  # the global th0 decision equals the whole-matrix decision (R-5)
+        assert same             # each shard's build is byte-identical to the oracle's
+    parts = next(p for _, _, _, p in res if p is not None)
+    y = np.concatenate([y for _, y in sorted(parts, key=lambda t: t[0])])
+    y_ref, _ = oracle.spmv_csr(A, synth.vector(A.n, synth.VEC_UNIFORM, seed=3))
+    assert np.array_equal(y, y_ref)  # row shards compute exactly the rows of the full product
+
+
+def _pi_worker(rank, world, port, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.uniform(4096, 4096, 50, 51, val_mode=1)
+        cuts = cbd.equal_bounds(A.m, world)
+        S = cbd.slice_rows(A, int(cuts[rank]), int(cuts[rank + 1]))
+
+        def spmv_scaled(x, ss, y):  # oracle stand-in for cbspmv_spmv_scaled
+            xs = x.numpy() / np.sqrt(ss.item())
+            y.copy_(torch.from_numpy(oracle.spmv_csr(S, xs)[0]))
+
+        def sumsq(y, out):
+            out.fill_(float(torch.dot(y, y)))
+
+        def all_reduce_sum(t):
+            dist.all_reduce(t)
+
+        def all_gather(out, inp):
+            parts = [torch.empty_like(inp) for _ in range(world)]
+            dist.all_gather(parts, inp)
+            out.copy_(torch.cat(parts))
+
+        x = torch.ones(A.n, dtype=torch.float64)
+        y = torch.empty(S.m, dtype=torch.float64)
+        ss = torch.tensor([float(A.n)], dtype=torch.float64)
+        lams = []
+        pi = cbd.PowerIteration(spmv_scaled, sumsq, all_reduce_sum, all_gather)
+        pi.run(x, y, ss, steps, on_step=lambda k, x, y, s: lams.append(float(np.sqrt(s.item()))))
+        q.put((rank, lams, x.numpy() if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_power_iteration_matches_single_process():
+    steps = 25
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_pi_worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # single-process reference: the same recurrence on the whole matrix with numpy
+    A = synth.uniform(4096, 4096, 50, 51, val_mode=1)
+    d = A.to_dense()
+    x = np.ones(A.n)
+    ss = float(A.n)
+    lam_ref = []
+    for _ in range(steps):
+        y = d @ (x / np.sqrt(ss))
+        ss = float(y @ y)
+        x = y
+        lam_ref.append(np.sqrt(ss))
+    assert res[0][1] == res[1][1]  # every rank sees the same all-reduced norm
+    assert np.allclose(res[0][1], lam_ref, rtol=1e-12)
+    assert np.allclose(res[0][2], x, rtol=1e-11)
+    # Perron root of a nonnegative matrix with row sums in [?]: bounded by min / max row sums
+    rs = d.sum(1)
+    assert rs.min() - 1e-9 <= lam_ref[-1] <= rs.max() + 1e-9
