@@ -536,7 +536,17 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
           const uint32_t *seg = c.restore.data() + c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk;
           std::memcpy(page + pos, seg, (size_t)ncol[i] * 4);
         }
-        std::memcpy(page + body, c.mtx.data() + c.vp[i], (size_t)canon_record_bytes(c, i));
+        if (type == CBSPMV_FMT_DENSE && c.blk == 16) {
+          // lane-major device layout: slot k*32 + l holds A[l % 16][(l / 16) * 8 + k]
+          const uint8_t *src = c.mtx.data() + c.vp[i];
+          for (int k = 0; k < 8; k++)
+            for (int l = 0; l < 32; l++) {
+              const int a = (l & 15) * 16 + (l >> 4) * 8 + k;
+              std::memcpy(page + body + (int64_t)(k * 32 + l) * S, src + (int64_t)a * S, (size_t)S);
+            }
+        } else {
+          std::memcpy(page + body, c.mtx.data() + c.vp[i], (size_t)canon_record_bytes(c, i));
+        }
         pos += rec[i];
       }
     }

@@ -63,7 +63,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_addr(bar)), "r"(parity)
@@ -266,44 +266,35 @@ __device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, co
   if (h == 0 && hi > lo) red_add(y + d.x + r, acc, dbg);
 }
 
-// DENSE (Alg. 4): element k*32 + lane is (row 2k + lane/16, col lane%16); a transposing
-// xor-butterfly (8, 4, 2, 1) leaves the full sum of row 2*((lane>>1)&7) + lane/16 in lane pairs.
+// DENSE (Alg. 4): the device record stores the 256 values lane-major: slot
+// k*32 + lane holds A[lane % 16][(lane / 16) * 8 + k], so lane l owns row l % 16, columns
+// 8*(l/16) .. +7 — conflict-free 8-byte shared loads, 8 FMAs against the broadcast x tile, one
+// shfl_xor(16) joins the two half rows (the semantics of Alg. 4's shfl, R-15), 16 REDs.
 template <typename V, bool SCALED>
 __device__ __forceinline__ void dense_path(const uint8_t *page, const uint4 &d, const V *xt, V scale,
                                            V *__restrict__ y, int64_t m, int lane, Dbg dbg) {
   const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
-  V xl = (lane & 15) < d_ncols(d) ? xt[lane & 15] : V(0);
-  if constexpr (SCALED) xl *= scale;
-  V p[8];
+  const int h = lane >> 4, r = lane & 15, nc = d_ncols(d);
+  // absent entries (stored zeros) must contribute 0 even against non-finite x: check the tile once
+  const bool finite = __all_sync(kFull, r >= nc || isfinite(xt[r]));
+  V acc = V(0);
+  if (finite) {
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const V v = vals[k * 32 + lane];
-    p[k] = v != V(0) ? v * xl : V(0);  // absent entries contribute 0 (explicit zeros were dropped)
-  }
-  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-  V q[4];
+    for (int k = 0; k < 8; k++) {
+      const int c = h * 8 + k;
+      acc = fma(vals[k * 32 + lane], c < nc ? xt[c] : V(0), acc);
+    }
+  } else {
 #pragma unroll
-  for (int j = 0; j < 4; j++) {
-    const V send = b3 ? p[j] : p[j + 4];
-    const V keep = b3 ? p[j + 4] : p[j];
-    q[j] = keep + __shfl_xor_sync(kFull, send, 8);
+    for (int k = 0; k < 8; k++) {
+      const V v = vals[k * 32 + lane];
+      const int c = h * 8 + k;
+      if (v != V(0)) acc = fma(v, xt[c], acc);
+    }
   }
-  V r2[2];
-#pragma unroll
-  for (int j = 0; j < 2; j++) {
-    const V send = b2 ? q[j] : q[j + 2];
-    const V keep = b2 ? q[j + 2] : q[j];
-    r2[j] = keep + __shfl_xor_sync(kFull, send, 4);
-  }
-  V s;
-  {
-    const V send = b1 ? r2[0] : r2[1];
-    const V keep = b1 ? r2[1] : r2[0];
-    s = keep + __shfl_xor_sync(kFull, send, 2);
-  }
-  s += __shfl_xor_sync(kFull, s, 1);
-  const int row = 2 * ((lane >> 1) & 7) + (lane >> 4);
-  if ((lane & 1) == 0 && (int64_t)d.x + row < m) red_add(y + d.x + row, s, dbg);
+  acc += __shfl_xor_sync(kFull, acc, 16);
+  if constexpr (SCALED) acc *= scale;
+  if (h == 0 && (int64_t)d.x + r < m) red_add(y + d.x + r, acc, dbg);
 }
 
 // ------------------------------------------------------------------ the persistent kernel

@@ -239,7 +239,12 @@ def test_device_stream_encodes_canonical_format(name):
             assert np.array_equal(rest, ex["restore_cols"][seg0:seg0 + b["ncols"]])
         else:
             assert b["xinfo"] == 16 * bc and b["ncols"] == min(16, A.n - 16 * bc)
-        assert np.array_equal(pg[b["body"]:b["body"] + size], ex["mtx_data"][vp:vp + size])
+        dev_rec = pg[b["body"]:b["body"] + size]
+        if typ == 2:  # lane-major dense layout: slot k*32 + l holds A[l % 16][(l // 16) * 8 + k]
+            k, l = np.divmod(np.arange(256), 32)
+            src = (l % 16) * 16 + (l // 16) * 8 + k
+            dev_rec = dev_rec.view(np.float64)[np.argsort(src)].view(np.uint8)
+        assert np.array_equal(dev_rec, ex["mtx_data"][vp:vp + size])
 
 
 @pytest.mark.parametrize("segred", ["0", "1"])
