@@ -360,6 +360,83 @@ def measure_also(names, dtype, steps, warmup, local_rank):
     return out
 
 
+def run_power(args, rank, world, local_rank):
+    """BASELINE configs[4]: iterated SpMV (power iteration) on the uniform matrix, rows split in
+    equal shards across ranks; a step = spmv_scaled + sumsq + (N>1) NCCL all-reduce + all-gather."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2605_18515_b200 as cb
+    from paper_2605_18515_b200 import dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    t0 = time.perf_counter()
+    A, (r0, r1), nnz_total = make_matrix("uniform", rank, world)
+    gen_s = time.perf_counter() - t0
+    agg = dist.global_agg(A, lambda a: _allreduce_np(a, dev, world), dtype=args.dtype) if world > 1 else -1
+    h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0)
+    info = h.info
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    x0 = torch.ones(A.n, dtype=tdt, device=dev)
+    dist.power_iteration_device(h, x0, max(args.warmup, 3), world)
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(st)
+        x, ss = dist.power_iteration_device(h, x0, args.steps, world)
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = float(_allreduce_np(np.array([ms]), dev, world, "max")[0])
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    y = torch.empty(A.m, dtype=tdt, device=dev)
+    k0.record(st)
+    for _ in range(args.steps):
+        cb.spmv_add(h, x0, y)
+    k1.record(st)
+    torch.cuda.synchronize()
+    kernel_ms = k0.elapsed_time(k1) / args.steps
+    lam = float(ss.item()) ** 0.5
+    peak, peak_src = peaks()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": 2.0 * nnz_total / (ms_max * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded generators, synth/)",
+            "config": {"workload": "BASELINE configs[4]: power iteration on uniform 2^25 x 2^25, 50 nnz/row",
+                       "name": "uniform", "nnz": int(nnz_total), "rows_per_rank": int(A.m), "agg": int(info["agg"]),
+                       "lambda": lam, "gen_s": gen_s, "build_s": info["build_seconds"],
+                       "parallelism": f"row-shard x{world}, NCCL all-reduce + all-gather per step"},
+            "roofline": {"bound": "hbm", "achieved": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9 / peak,
+                         "traffic": ncu_traffic("uniform", args.dtype), "kernel": "cb_spmv_kernel",
+                         "kernel_ms": kernel_ms, "peak_source": peak_src},
+            "gpu_launches": int(args.steps * (2 + 1)),
+            "clocks": clk.summary(), "cpu_baseline": None,
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    cb.destroy(h)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def _allreduce_np(a, dev, world, op="sum"):
+    if world == 1:
+        return np.asarray(a)
+    import torch
+    import torch.distributed as tdist
+    t = torch.from_numpy(np.asarray(a)).to(dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.SUM if op == "sum" else tdist.ReduceOp.MAX)
+    return t.cpu().numpy()
+
+
 def cpu_baseline(A, x, dtype):
     """The oracle as it stands (single-threaded C, Alg. 1) on a bounded sample: ~10 s of CPU work."""
     import oracle
@@ -406,6 +483,8 @@ def main():
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.config == "uniform":
+        run_power(args, rank, world, local_rank)
     else:
         run_cb(args, rank, world, local_rank)
 

@@ -88,3 +88,32 @@ class PowerIteration:
             if on_step is not None:
                 on_step(k, x, y, sumsq)
         return x, sumsq
+
+
+def power_iteration_device(h, x0, steps: int, world: int = 1, group=None, on_step=None):
+    """BASELINE configs[4] on the device: y_k = A_shard (x_k / ||x_k||) through
+    cbspmv_spmv_scaled (normalisation folded into the x load), sum(y_k^2) by
+    cbspmv_sumsq, then an NCCL all-reduce of the 8-byte sum and an all-gather of the
+    y shards into the next x (equal shards).  One rank owns rows
+    [rank*m/world, (rank+1)*m/world) of a square matrix; x0 is the full start vector.
+    Returns (x, sumsq) on the device; lambda_k = sqrt(sumsq_k)."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2605_18515_b200 as cb
+    m_local = h.info["m"]
+    x = x0.clone()
+    y = torch.empty(m_local, dtype=x0.dtype, device=x0.device)
+    ss = torch.zeros(1, dtype=torch.float64, device=x0.device)
+    cb.sumsq(x, ss, device=x0.device.index)           # ||x_0||^2 (replicated x)
+    for k in range(steps):
+        cb.spmv_scaled(h, x, ss, y)                     # y = A (x / sqrt(ss))
+        cb.sumsq(y, ss, device=x0.device.index)         # local sum of squares
+        if world > 1:
+            tdist.all_reduce(ss, group=group)
+            tdist.all_gather_into_tensor(x, y, group=group)
+        else:
+            x, y = y, x                                 # the full y is the next x
+        if on_step is not None:
+            on_step(k, x, ss)
+    return x, ss

@@ -337,3 +337,38 @@ def test_x_not_16_byte_aligned(name):
     cb.spmv(h, xs, y)
     torch.cuda.synchronize()
     check_rows(y.cpu().numpy(), y_ref, R, 1e-12)
+
+
+def test_power_iteration_device_matches_recurrence():
+    """configs[4] driver (N=1): spmv_scaled + sumsq, step by step against the numpy recurrence."""
+    _ok()
+    from paper_2605_18515_b200 import dist as cbd
+    A = synth.uniform(1 << 13, 1 << 13, 50, 51, val_mode=1)
+    h = cb.build(A, device=0)
+    x0 = torch.ones(A.n, dtype=torch.float64, device=DEV)
+    lams = []
+    x, ss = cbd.power_iteration_device(h, x0, 30, on_step=lambda k, x, s: lams.append(float(s.item()) ** 0.5))
+    d = A.to_dense()
+    xr, ssr, ref = np.ones(A.n), float(A.n), []
+    for _ in range(30):
+        yr = d @ (xr / np.sqrt(ssr))
+        ssr = float(yr @ yr)
+        xr = yr
+        ref.append(np.sqrt(ssr))
+    assert np.allclose(lams, ref, rtol=1e-12)
+    assert np.allclose(x.cpu().numpy(), xr, rtol=1e-11, atol=0)
+    rs = d.sum(1)
+    assert rs.min() - 1e-9 <= lams[-1] <= rs.max() + 1e-9
+
+
+def test_power_iteration_exact_ones_fixed_point():
+    """All-ones values, exactly 50 per row, n = 4096: every quantity is a dyadic rational
+    (1/64, 50/64, 2500), so lambda = 50 exactly at every step, in any summation order."""
+    _ok()
+    from paper_2605_18515_b200 import dist as cbd
+    A = synth.uniform(1 << 12, 1 << 12, 50, 51, val_mode=3)
+    h = cb.build(A, device=0)
+    lams = []
+    cbd.power_iteration_device(h, torch.ones(A.n, dtype=torch.float64, device=DEV), 10,
+                               on_step=lambda k, x, s: lams.append(float(s.item()) ** 0.5))
+    assert lams == [50.0] * 10
