@@ -65,6 +65,11 @@ typedef struct {
   int32_t device;         /* CUDA ordinal for the device copy; -1 = host-only build (export/info only) */
   int32_t host_threads;   /* host builder threads; 0 = all online cores */
   int32_t keep_host;      /* 1 = keep the canonical host arrays for cbspmv_export (default 1) */
+  int32_t col_panels;     /* column panels (NEXT-1): 0 = auto (x larger than 3/4 of L2 ->
+                             panels of <= 3/8 L2 of x each), 1 = none, k >= 2 = k panels.  Each panel
+                             (all rows, columns [c_k, c_k+1), 16-aligned) runs the whole pipeline as
+                             its own matrix; cbspmv_spmv zeroes y once and runs the panels in order so
+                             each panel's slice of x stays L2-resident. */
 } cbspmv_options_t;
 
 typedef struct {
@@ -93,6 +98,7 @@ typedef struct {
   int32_t launches_per_spmv;      /* kernels launched by one cbspmv_spmv */
   double build_seconds;           /* host pipeline wall time (a1..a7 + device layout) */
   double upload_seconds;          /* H2D copy wall time */
+  int32_t n_panels;               /* column panels (1 = whole matrix); counts above sum over panels */
 } cbspmv_info_t;
 
 /* Host copies of the canonical format, slot order (after Alg. 2).  Pointers
@@ -170,12 +176,14 @@ cbspmv_status_t cbspmv_decide_agg(int64_t nb_pre, int64_t ss_count, const cbspmv
 
 cbspmv_status_t cbspmv_get_info(cbspmv_handle_t h, cbspmv_info_t *info);
 
-/* Canonical format (requires keep_host = 1). */
+/* Canonical format (requires keep_host = 1).  With column panels this is panel 0; use
+ * cbspmv_export_panel for panel k (0 <= k < info.n_panels). */
 cbspmv_status_t cbspmv_export(cbspmv_handle_t h, cbspmv_export_t *ex);
+cbspmv_status_t cbspmv_export_panel(cbspmv_handle_t h, int32_t k, cbspmv_export_t *ex);
 
 /* Copy the device page stream (dev_stream_bytes) and page offsets
  * (n_pages + 1 uint64) back to host buffers of at least that size (layout
- * verification; synchronous). */
+ * verification; synchronous; single-panel handles only). */
 cbspmv_status_t cbspmv_download_stream(cbspmv_handle_t h, void *stream_host, size_t stream_bytes,
                                        uint64_t *page_off_host, size_t n_page_off);
 

@@ -37,7 +37,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSORTED", 3: "ENOMEM", 4: "ECUDA", 5: "EDI
 class Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32)] + [(k, ctypes.c_int32) for k in (
         "blk", "th0_num", "th0_den", "ss_limit", "th1", "th2", "warps_per_tb", "agg_mode", "balance",
-        "force_format", "device", "host_threads", "keep_host")]
+        "force_format", "device", "host_threads", "keep_host", "col_panels")]
 
 
 class Info(ctypes.Structure):
@@ -51,7 +51,7 @@ class Info(ctypes.Structure):
         ("meta_bytes", ctypes.c_int64), ("alg_bytes", ctypes.c_int64), ("dev_stream_bytes", ctypes.c_int64),
         ("n_pages", ctypes.c_int64), ("dev_bytes", ctypes.c_int64), ("grid", ctypes.c_int32),
         ("launches_per_spmv", ctypes.c_int32), ("build_seconds", ctypes.c_double),
-        ("upload_seconds", ctypes.c_double),
+        ("upload_seconds", ctypes.c_double), ("n_panels", ctypes.c_int32),
     ]
 
 
@@ -90,6 +90,7 @@ def lib():
             "cbspmv_decide_agg": ([i64, i64, ctypes.POINTER(Options), ctypes.POINTER(i32)], i32),
             "cbspmv_get_info": ([H, ctypes.POINTER(Info)], i32),
             "cbspmv_export": ([H, ctypes.POINTER(Export)], i32),
+            "cbspmv_export_panel": ([H, i32, ctypes.POINTER(Export)], i32),
             "cbspmv_download_stream": ([H, vp, ctypes.c_size_t, vp, ctypes.c_size_t], i32),
             "cbspmv_destroy": ([H], i32),
             "cbspmv_status_string": ([i32], ctypes.c_char_p),
@@ -244,10 +245,10 @@ def get_info(h: Handle) -> dict:
     return d
 
 
-def export(h: Handle) -> dict:
-    """Host copies of the canonical format (slot order) as numpy arrays."""
+def export(h: Handle, panel: int = 0) -> dict:
+    """Host copies of the canonical format (slot order) of column panel `panel` as numpy arrays."""
     e = Export()
-    _check(lib().cbspmv_export(h.raw, ctypes.byref(e)), "cbspmv_export")
+    _check(lib().cbspmv_export_panel(h.raw, panel, ctypes.byref(e)), "cbspmv_export_panel")
 
     def arr(p, n, dt):
         if n == 0 or not p:

@@ -230,6 +230,12 @@ void pre_stats(const Csr &A, const cbspmv_options_t &o, int64_t blk_m, std::vect
 
 }  // namespace
 
+int check_csr(const Csr &A, const cbspmv_options_t &o, int64_t *nnz, std::string *err) {
+  int st = check_options(A, o, err);
+  if (st != CBSPMV_OK) return st;
+  return canonical_check(A, o.host_threads, nnz, err);
+}
+
 bool decide_agg(int64_t nb_pre, int64_t ss_count, const cbspmv_options_t &o) {
   // aggregate iff ss / nb >= th0_num / th0_den, compared exactly in integers (R-3, R-5)
   return nb_pre > 0 && ss_count * (int64_t)o.th0_den >= (int64_t)o.th0_num * nb_pre;

@@ -27,12 +27,13 @@ double now() {
 
 struct DeviceGuard {  // switch to the handle's device for the call, restore afterwards
   int prev = -1, want;
-  explicit DeviceGuard(int d) : want(d) {
+  explicit DeviceGuard(int d) : want(d) {  // d < 0: host-only, no-op
+    if (want < 0) return;
     if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
     if (prev != want) cudaSetDevice(want);
   }
   ~DeviceGuard() {
-    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+    if (want >= 0 && prev >= 0 && prev != want) cudaSetDevice(prev);
   }
 };
 
@@ -47,6 +48,24 @@ void load_stats(const std::vector<int64_t> &v, double *mean, double *sd, int64_t
   *mx = M;
 }
 
+// One column panel: the CB-SpMV format of A[:, c0:c1) and its device copy.
+struct Part {
+  int64_t c0 = 0, c1 = 0;
+  cb::Canon canon;
+  CbDevice dev;
+  uint8_t *d_stream = nullptr;
+  uint64_t *d_page_off = nullptr;
+  uint32_t *d_cta_page = nullptr;
+  int64_t stream_bytes = 0, n_pages = 0;
+};
+
+// Rows x columns [c0, c1) of a canonical CSR (columns keep their global index).
+struct SubCsr {
+  std::vector<int64_t> rp;
+  std::vector<int32_t> col;
+  std::vector<uint8_t> val;  // raw bytes of the value type
+};
+
 }  // namespace
 
 struct cbspmv_s {
@@ -54,12 +73,8 @@ struct cbspmv_s {
   int dtype = CBSPMV_F64;
   int val_size = 8;
   bool has_host = false;
-  cb::Canon canon;
+  std::vector<Part> parts;
   cbspmv_info_t info{};
-  CbDevice dev;
-  uint8_t *d_stream = nullptr;
-  uint64_t *d_page_off = nullptr;
-  uint32_t *d_cta_page = nullptr;
   void *d_x_tmp = nullptr;
   void *d_y_tmp = nullptr;
 };
@@ -83,19 +98,80 @@ cbspmv_status_t cbspmv_default_options(cbspmv_options_t *o) {
   o->device = 0;
   o->host_threads = 0;
   o->keep_host = 1;
+  o->col_panels = 0;
   return CBSPMV_OK;
 }
 
 static void free_device(cbspmv_s *h) {
   if (h->device < 0) return;
   DeviceGuard g(h->device);
-  cudaFree(h->d_stream);
-  cudaFree(h->d_page_off);
-  cudaFree(h->d_cta_page);
+  for (Part &p : h->parts) {
+    cudaFree(p.d_stream);
+    cudaFree(p.d_page_off);
+    cudaFree(p.d_cta_page);
+    p.d_stream = nullptr; p.d_page_off = nullptr; p.d_cta_page = nullptr;
+  }
   cudaFree(h->d_x_tmp);
   cudaFree(h->d_y_tmp);
-  h->d_stream = nullptr; h->d_page_off = nullptr; h->d_cta_page = nullptr;
   h->d_x_tmp = nullptr; h->d_y_tmp = nullptr;
+}
+
+// Build + upload one panel's format (the Fig. 7 pipeline on A[:, c0:c1)).
+static int build_part(const cb::Csr &A, const cbspmv_options_t &o, cudaStream_t cs, Part *P, double *t_up,
+                      std::string *err) {
+  int st = cb::build_canonical(A, o, &P->canon, err);
+  if (st != CBSPMV_OK || o.device < 0) return st;
+  const cb::Canon &c = P->canon;
+  cb::Stream S;
+  const char *env = std::getenv("CBSPMV_PAGE_BYTES");
+  int cap = env ? std::atoi(env) : cb::kDefaultStageCap;
+  cap = (int)cb::round_up(std::max(cap, 1024), 16);
+  st = cb::build_stream(c, cap, o.host_threads, &S, err);
+  if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
+  const int64_t npages = (int64_t)S.page_off.size() - 1;
+  CbDevice &D = P->dev;
+  D.device = o.device; D.dtype = A.val_size == 8 ? CBSPMV_F64 : CBSPMV_F32; D.agg = c.agg; D.m = c.m; D.n = c.n;
+  D.n_pages = npages; D.page_cap = cap;
+  st = cb_configure(&D, err);
+  if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
+  // persistent CTA g streams pages [cta[g], cta[g+1]): equal byte shares
+  std::vector<uint32_t> cta(D.grid + 1, 0);
+  const uint64_t total = S.page_off.back();
+  for (int g = 1; g < D.grid; g++) {
+    uint64_t target = total / D.grid * g + (total % D.grid) * g / D.grid;
+    cta[g] = (uint32_t)(std::lower_bound(S.page_off.begin(), S.page_off.end() - 1, target) - S.page_off.begin());
+  }
+  cta[D.grid] = (uint32_t)npages;
+  const double t1 = now();
+  cudaError_t e = cudaSuccess;
+  if (S.nbytes > 0) e = cudaMalloc(&P->d_stream, (size_t)S.nbytes);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_page_off, S.page_off.size() * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_cta_page, cta.size() * sizeof(uint32_t));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cb::free_stream(&S);
+    *err = std::string("device allocation: ") + cudaGetErrorString(e);
+    return CBSPMV_ENOMEM;
+  }
+  // "transferred to the GPU in a single operation"
+  if (S.nbytes > 0) e = cudaMemcpyAsync(P->d_stream, S.bytes, (size_t)S.nbytes, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(P->d_page_off, S.page_off.data(), S.page_off.size() * sizeof(uint64_t),
+                        cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(P->d_cta_page, cta.data(), cta.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  cb::free_stream(&S);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *err = std::string("upload: ") + cudaGetErrorString(e);
+    return CBSPMV_ECUDA;
+  }
+  *t_up += now() - t1;
+  D.d_stream = P->d_stream; D.d_page_off = P->d_page_off; D.d_cta_page = P->d_cta_page;
+  P->stream_bytes = (int64_t)total;
+  P->n_pages = npages;
+  return CBSPMV_OK;
 }
 
 cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
@@ -115,102 +191,124 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
   if (o.device >= 0 && o.blk != 16) return fail(CBSPMV_EUNSUPPORTED, "device kernels require blk = 16");
   if (o.device >= 0 && m > (int64_t)UINT32_MAX)
     return fail(CBSPMV_EUNSUPPORTED, "m too large for 32-bit block row offsets");
+  if (o.col_panels < 0) return fail(CBSPMV_EINVAL, "col_panels must be >= 0");
 
   cbspmv_s *h = new (std::nothrow) cbspmv_s();
   if (!h) return fail(CBSPMV_ENOMEM, "handle allocation");
   h->dtype = dtype;
   h->val_size = dtype == CBSPMV_F64 ? 8 : 4;
-
-  const double t0 = now();
-  cb::Csr A{m, n, nnz, row_ptr, col_idx, vals, h->val_size};
-  std::string err;
-  int st = cb::build_canonical(A, o, &h->canon, &err);
-  if (st != CBSPMV_OK) { delete h; return fail(st, err); }
-  const cb::Canon &c = h->canon;
-
-  cbspmv_info_t &I = h->info;
-  I.m = c.m; I.n = c.n; I.nnz = c.nnz; I.blk_m = c.blk_m; I.nb = c.nb; I.nb_pre = c.nb_pre;
-  I.ss_count = c.ss_count; I.agg = c.agg; I.dtype = dtype;
-  for (int k = 0; k < 3; k++) I.fmt_count[k] = c.fmt_count[k];
-  I.T = c.T;
-  load_stats(c.tb_load, &I.tb_load_mean, &I.tb_load_sd, &I.tb_load_max);
-  double mu_nat;
-  load_stats(c.tb_load_nat, &mu_nat, &I.tb_load_sd_natural, &I.tb_load_max_natural);
-  I.mtx_bytes = (int64_t)c.mtx.size();
-  I.n_restore = (int64_t)c.restore.size();
-  I.meta_bytes = 21 * c.nb;
-  I.alg_bytes = I.meta_bytes + I.mtx_bytes + 4 * I.n_restore + (c.agg ? 8 * (c.blk_m + 1) : 0) +
-                (int64_t)h->val_size * (c.n + c.m);
-
+  const int S = h->val_size;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (o.device >= 0) {
-    h->device = o.device;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || o.device >= ndev) {
       cudaGetLastError();
       delete h;
       return fail(CBSPMV_ECUDA, "no CUDA device " + std::to_string(o.device));
     }
-    DeviceGuard g(h->device);
-    cb::Stream S;
-    const char *env = std::getenv("CBSPMV_PAGE_BYTES");
-    int cap = env ? std::atoi(env) : cb::kDefaultStageCap;
-    cap = (int)cb::round_up(std::max(cap, 1024), 16);
-    st = cb::build_stream(c, cap, o.host_threads, &S, &err);
-    if (st != CBSPMV_OK) { cb::free_stream(&S); delete h; return fail(st, err); }
-    I.build_seconds = now() - t0;
-    const int64_t npages = (int64_t)S.page_off.size() - 1;
-    CbDevice &D = h->dev;
-    D.device = h->device; D.dtype = dtype; D.agg = c.agg; D.m = c.m; D.n = c.n;
-    D.n_pages = npages; D.page_cap = cap;
-    st = cb_configure(&D, &err);
-    if (st != CBSPMV_OK) { cb::free_stream(&S); delete h; return fail(st, err); }
-    // persistent CTA c streams pages [cta_page[c], cta_page[c+1]): equal byte shares
-    std::vector<uint32_t> cta(D.grid + 1, 0);
-    const uint64_t total = S.page_off.back();
-    for (int g2 = 1; g2 < D.grid; g2++) {
-      uint64_t target = total / D.grid * g2 + (total % D.grid) * g2 / D.grid;
-      cta[g2] = (uint32_t)(std::lower_bound(S.page_off.begin(), S.page_off.end() - 1, target) - S.page_off.begin());
-    }
-    cta[D.grid] = (uint32_t)npages;
-    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-    const double t1 = now();
-    cudaError_t e = cudaSuccess;
-    if (S.nbytes > 0) e = cudaMalloc(&h->d_stream, (size_t)S.nbytes);
-    if (e == cudaSuccess) e = cudaMalloc(&h->d_page_off, S.page_off.size() * sizeof(uint64_t));
-    if (e == cudaSuccess) e = cudaMalloc(&h->d_cta_page, cta.size() * sizeof(uint32_t));
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      cb::free_stream(&S); free_device(h); delete h;
-      return fail(CBSPMV_ENOMEM, std::string("device allocation: ") + cudaGetErrorString(e));
-    }
-    // "transferred to the GPU in a single operation"
-    if (S.nbytes > 0) e = cudaMemcpyAsync(h->d_stream, S.bytes, (size_t)S.nbytes, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(h->d_page_off, S.page_off.data(), S.page_off.size() * sizeof(uint64_t),
-                          cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(h->d_cta_page, cta.data(), cta.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
-    cb::free_stream(&S);
-    if (e != cudaSuccess) {
-      cudaGetLastError(); free_device(h); delete h;
-      return fail(CBSPMV_ECUDA, std::string("upload: ") + cudaGetErrorString(e));
-    }
-    I.upload_seconds = now() - t1;
-    D.d_stream = h->d_stream; D.d_page_off = h->d_page_off; D.d_cta_page = h->d_cta_page;
-    I.dev_stream_bytes = (int64_t)total;
-    I.n_pages = npages;
-    I.dev_bytes = (int64_t)total + (int64_t)(npages + 1) * 8 + (int64_t)cta.size() * 4;
-    I.grid = D.grid;
-    I.launches_per_spmv = (c.m > 0 ? 1 : 0) + (npages > 0 ? 1 : 0);
-  } else {
-    I.build_seconds = now() - t0;
+    h->device = o.device;
   }
+  DeviceGuard guard(o.device);
+
+  const double t0 = now();
+  cb::Csr A{m, n, nnz, row_ptr, col_idx, vals, S};
+  std::string err;
+  // column panels (NEXT-1): decided from x's size against the device L2
+  int P = o.col_panels;
+  if (P == 0) {
+    P = 1;
+    if (o.device >= 0) {
+      int l2 = 0;
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, o.device);
+      const double xb = (double)n * S;
+      if (l2 > 0 && xb > 0.75 * l2) P = (int)std::ceil(xb / (0.375 * l2));
+    }
+  }
+  const int64_t nbc = (n + o.blk - 1) / o.blk;
+  P = (int)std::max<int64_t>(1, std::min<int64_t>(P, nbc));
+  std::vector<int64_t> cuts(P + 1);
+  for (int k = 0; k <= P; k++) cuts[k] = std::min<int64_t>(n, (nbc * k / P) * o.blk);
+  cuts[P] = n;
+  double t_up = 0.0;
+  int st = CBSPMV_OK;
+  h->parts.resize(P);
+  if (P == 1) {
+    h->parts[0].c0 = 0; h->parts[0].c1 = n;
+    st = build_part(A, o, cs, &h->parts[0], &t_up, &err);
+  } else {
+    int64_t nz = 0;
+    st = cb::check_csr(A, o, &nz, &err);  // the split below relies on sorted, in-range columns
+    for (int k = 0; k < P && st == CBSPMV_OK; k++) {
+      SubCsr sub;
+      sub.rp.assign((size_t)m + 1, 0);
+      const int64_t c0 = cuts[k], c1 = cuts[k + 1];
+      std::vector<int64_t> lo(m), hi(m);
+      cb::parallel_for(m, o.host_threads, 1 << 14, [&](int64_t a, int64_t b, int) {
+        for (int64_t i = a; i < b; i++) {
+          const int32_t *rb = col_idx + row_ptr[i], *re = col_idx + row_ptr[i + 1];
+          lo[i] = std::lower_bound(rb, re, (int32_t)c0) - col_idx;
+          hi[i] = std::lower_bound(rb, re, (int32_t)std::min<int64_t>(c1, INT32_MAX)) - col_idx;
+        }
+      });
+      for (int64_t i = 0; i < m; i++) sub.rp[i + 1] = sub.rp[i] + (hi[i] - lo[i]);
+      const int64_t snz = sub.rp[m];
+      sub.col.resize((size_t)std::max<int64_t>(snz, 1));
+      sub.val.resize((size_t)std::max<int64_t>(snz, 1) * S);
+      cb::parallel_for(m, o.host_threads, 1 << 14, [&](int64_t a, int64_t b, int) {
+        for (int64_t i = a; i < b; i++) {
+          const int64_t len = hi[i] - lo[i];
+          std::memcpy(sub.col.data() + sub.rp[i], col_idx + lo[i], (size_t)len * 4);
+          std::memcpy(sub.val.data() + sub.rp[i] * S, (const uint8_t *)vals + lo[i] * S, (size_t)len * S);
+        }
+      });
+      cb::Csr Ak{m, n, snz, sub.rp.data(), sub.col.data(), sub.val.data(), S};
+      h->parts[k].c0 = c0; h->parts[k].c1 = c1;
+      st = build_part(Ak, o, cs, &h->parts[k], &t_up, &err);
+    }
+  }
+  if (st != CBSPMV_OK) { free_device(h); delete h; return fail(st, err); }
+
+  // info: sums over panels
+  cbspmv_info_t &I = h->info;
+  I.m = m; I.n = n; I.dtype = dtype; I.n_panels = P;
+  std::vector<int64_t> loads, loads_nat;
+  for (const Part &p : h->parts) {
+    const cb::Canon &c = p.canon;
+    I.nnz += c.nnz; I.nb += c.nb; I.nb_pre += c.nb_pre; I.ss_count += c.ss_count; I.agg |= c.agg;
+    I.blk_m = c.blk_m;
+    for (int k = 0; k < 3; k++) I.fmt_count[k] += c.fmt_count[k];
+    I.T += c.T;
+    I.mtx_bytes += (int64_t)c.mtx.size();
+    I.n_restore += (int64_t)c.restore.size();
+    I.meta_bytes += 21 * c.nb;
+    I.alg_bytes += 21 * c.nb + (int64_t)c.mtx.size() + 4 * (int64_t)c.restore.size() + (c.agg ? 8 * (c.blk_m + 1) : 0);
+    loads.insert(loads.end(), c.tb_load.begin(), c.tb_load.end());
+    loads_nat.insert(loads_nat.end(), c.tb_load_nat.begin(), c.tb_load_nat.end());
+    I.dev_stream_bytes += p.stream_bytes;
+    I.n_pages += p.n_pages;
+    I.dev_bytes += p.stream_bytes + (p.n_pages + 1) * 8 + (int64_t)(p.dev.grid + 1) * 4;
+    I.launches_per_spmv += p.n_pages > 0 ? 1 : 0;
+  }
+  I.alg_bytes += (int64_t)S * (n + m);
+  load_stats(loads, &I.tb_load_mean, &I.tb_load_sd, &I.tb_load_max);
+  double mu_nat;
+  load_stats(loads_nat, &mu_nat, &I.tb_load_sd_natural, &I.tb_load_max_natural);
+  if (h->device >= 0) {
+    I.grid = h->parts[0].dev.grid;
+    if (m > 0) I.launches_per_spmv += 1;  // the y-zeroing kernel
+  } else {
+    I.launches_per_spmv = 0;
+  }
+  I.upload_seconds = t_up;
+  I.build_seconds = now() - t0 - t_up;
   h->has_host = o.keep_host != 0;
   if (!h->has_host) {
-    cb::Canon small;
-    small.m = c.m; small.n = c.n; small.nnz = c.nnz; small.nb = c.nb; small.T = c.T;
-    h->canon = std::move(small);
+    for (Part &p : h->parts) {
+      cb::Canon small;
+      small.m = p.canon.m; small.n = p.canon.n; small.nnz = p.canon.nnz; small.nb = p.canon.nb;
+      small.T = p.canon.T; small.agg = p.canon.agg; small.blk_m = p.canon.blk_m;
+      p.canon = std::move(small);
+    }
   }
   *out = h;
   g_err.clear();
@@ -227,12 +325,25 @@ static cbspmv_status_t check_dev(cbspmv_handle_t h, const void *x, const void *y
   return CBSPMV_OK;
 }
 
+// y (+)= A·(s·x): the panels run in order, the first launch zeroes y when asked.
+static int launch_all(cbspmv_handle_t h, const void *x, void *y, const double *ss, bool zero, void *stream,
+                      std::string *err) {
+  bool first = true;
+  for (const Part &p : h->parts) {
+    if (p.n_pages == 0 && !(first && zero)) continue;
+    int st = cb_launch_spmv(p.dev, x, y, ss, first && zero, stream, err);
+    if (st != CBSPMV_OK) return st;
+    first = false;
+  }
+  return CBSPMV_OK;
+}
+
 static cbspmv_status_t run(cbspmv_handle_t h, const void *x, void *y, const double *ss, bool zero, void *stream) {
   cbspmv_status_t s = check_dev(h, x, y);
   if (s != CBSPMV_OK) return s;
   DeviceGuard g(h->device);
   std::string err;
-  int st = cb_launch_spmv(h->dev, x, y, ss, zero, stream, &err);
+  int st = launch_all(h, x, y, ss, zero, stream, &err);
   if (st != CBSPMV_OK) return fail(st, err);
   return CBSPMV_OK;
 }
@@ -264,7 +375,7 @@ cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_
   if (xb) e = cudaMemcpyAsync(h->d_x_tmp, x_host, xb, cudaMemcpyHostToDevice, cs);
   if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ECUDA, cudaGetErrorString(e)); }
   std::string err;
-  int st = cb_launch_spmv(h->dev, h->d_x_tmp, h->d_y_tmp, nullptr, true, stream, &err);
+  int st = launch_all(h, h->d_x_tmp, h->d_y_tmp, nullptr, true, stream, &err);
   if (st != CBSPMV_OK) return fail(st, err);
   if (yb) e = cudaMemcpyAsync(y_host, h->d_y_tmp, yb, cudaMemcpyDeviceToHost, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
@@ -320,10 +431,11 @@ cbspmv_status_t cbspmv_get_info(cbspmv_handle_t h, cbspmv_info_t *info) {
   return CBSPMV_OK;
 }
 
-cbspmv_status_t cbspmv_export(cbspmv_handle_t h, cbspmv_export_t *ex) {
+cbspmv_status_t cbspmv_export_panel(cbspmv_handle_t h, int32_t k, cbspmv_export_t *ex) {
   if (!h || !ex) return fail(CBSPMV_EINVAL, "null argument");
+  if (k < 0 || k >= (int32_t)h->parts.size()) return fail(CBSPMV_EINVAL, "panel index out of range");
   if (!h->has_host) return fail(CBSPMV_EUNSUPPORTED, "built with keep_host = 0");
-  const cb::Canon &c = h->canon;
+  const cb::Canon &c = h->parts[k].canon;
   ex->nb = c.nb; ex->T = c.T; ex->mtx_bytes = (int64_t)c.mtx.size();
   ex->n_restore = (int64_t)c.restore.size(); ex->n_cols_offset = (int64_t)c.cols_offset.size();
   ex->blk_row_idx = c.br.data(); ex->blk_col_idx = c.bc.data(); ex->nnz_per_blk = c.nnzb.data();
@@ -334,18 +446,21 @@ cbspmv_status_t cbspmv_export(cbspmv_handle_t h, cbspmv_export_t *ex) {
   return CBSPMV_OK;
 }
 
+cbspmv_status_t cbspmv_export(cbspmv_handle_t h, cbspmv_export_t *ex) { return cbspmv_export_panel(h, 0, ex); }
+
 cbspmv_status_t cbspmv_download_stream(cbspmv_handle_t h, void *stream_host, size_t stream_bytes,
                                        uint64_t *page_off_host, size_t n_page_off) {
   if (!h) return fail(CBSPMV_EINVAL, "null handle");
   if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle");
-  if (stream_bytes < (size_t)h->info.dev_stream_bytes || n_page_off < (size_t)h->info.n_pages + 1)
+  if (h->parts.size() != 1) return fail(CBSPMV_EUNSUPPORTED, "multi-panel handle");
+  const Part &p = h->parts[0];
+  if (stream_bytes < (size_t)p.stream_bytes || n_page_off < (size_t)p.n_pages + 1)
     return fail(CBSPMV_EDIM, "destination too small");
   DeviceGuard g(h->device);
   cudaError_t e = cudaSuccess;
-  if (h->info.dev_stream_bytes)
-    e = cudaMemcpy(stream_host, h->d_stream, (size_t)h->info.dev_stream_bytes, cudaMemcpyDeviceToHost);
+  if (p.stream_bytes) e = cudaMemcpy(stream_host, p.d_stream, (size_t)p.stream_bytes, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess)
-    e = cudaMemcpy(page_off_host, h->d_page_off, ((size_t)h->info.n_pages + 1) * 8, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(page_off_host, p.d_page_off, ((size_t)p.n_pages + 1) * 8, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ECUDA, cudaGetErrorString(e)); }
   return CBSPMV_OK;
 }

@@ -71,6 +71,8 @@ struct Csr {
   int val_size;  // 8 = double, 4 = float
 };
 
+// a1 only (options + canonical check of the whole CSR).
+int check_csr(const Csr &A, const cbspmv_options_t &o, int64_t *nnz, std::string *err);
 // a1 + a3 only: canonical check and pre-aggregation block statistics.
 int block_stats(const Csr &A, const cbspmv_options_t &o, int64_t *nb_pre, int64_t *ss_count, std::string *err);
 bool decide_agg(int64_t nb_pre, int64_t ss_count, const cbspmv_options_t &o);

@@ -134,3 +134,31 @@ def test_info_bytes():
         + S * (i["n"] + i["m"])
     assert i["alg_bytes"] == expect
     assert i["meta_bytes"] == 21 * i["nb"]
+
+
+def panel_csr(A, c0, c1):
+    """Columns [c0, c1) of A with global column indices (test-side slicing)."""
+    rows = np.repeat(np.arange(A.m), np.diff(A.row_ptr))
+    keep = (A.col >= c0) & (A.col < c1)
+    rp = np.zeros(A.m + 1, np.int64)
+    np.add.at(rp, rows[keep] + 1, 1)
+    return synth.CSR(A.m, A.n, np.cumsum(rp), A.col[keep].copy(), A.val[keep].copy())
+
+
+@pytest.mark.parametrize("P", [2, 3, 7])
+def test_column_panels_each_equal_oracle(P):
+    """NEXT-1 column panels: every panel's format is the oracle's build of A[:, c_k:c_k+1)."""
+    A = synth.random_csr(200, 300, 0.08, 41, pattern="hub")
+    h = cb.build(A, device=-1, col_panels=P)
+    assert h.info["n_panels"] == P
+    nbc = (A.n + 15) // 16
+    cuts = [min(A.n, (nbc * k // P) * 16) for k in range(P)] + [A.n]
+    tot = 0
+    for k in range(P):
+        Ak = panel_csr(A, cuts[k], cuts[k + 1])
+        ref = oracle.build(Ak)
+        got = cb.export(h, panel=k)
+        for key in KEYS:
+            assert np.array_equal(got[key], getattr(ref, key)), (k, key)
+        tot += ref.nnz
+    assert tot == A.nnz == h.info["nnz"]

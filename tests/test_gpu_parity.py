@@ -372,3 +372,22 @@ def test_power_iteration_exact_ones_fixed_point():
     cbd.power_iteration_device(h, torch.ones(A.n, dtype=torch.float64, device=DEV), 10,
                                on_step=lambda k, x, s: lams.append(float(s.item()) ** 0.5))
     assert lams == [50.0] * 10
+
+
+@pytest.mark.parametrize("P", [2, 5])
+@pytest.mark.parametrize("name", ["rmat", "clustered", "uniform"])
+def test_column_panels_spmv(P, name):
+    """NEXT-1 column panels: y = sum over panels, zeroed once; scaled and add variants too."""
+    _ok()
+    A = synth.make(name, small=True)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=9)
+    y_ref, R = oracle.spmv_csr(A, x)
+    y, h = gpu_spmv(A, x, col_panels=P)
+    assert h.info["n_panels"] == P
+    check_rows(y, y_ref, R, 1e-12)
+    xd = torch.from_numpy(x).to(DEV)
+    ss = torch.tensor([4.0], dtype=torch.float64, device=DEV)
+    ys = torch.empty(A.m, dtype=torch.float64, device=DEV)
+    cb.spmv_scaled(h, xd, ss, ys)
+    torch.cuda.synchronize()
+    check_rows(ys.cpu().numpy() * 2.0, y_ref, R, 1e-12)
