@@ -428,14 +428,15 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
   parallel_for(c.nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
     for (int64_t i = lo; i < hi; i++) { int nc; rec[i] = dev_record_bytes(c, i, canon_record_bytes(c, i), &nc); ncol[i] = nc; }
   });
-  // Work items of a block range: COO groups (consecutive COO blocks, nnz sum <= 32) and
-  // single CSR / DENSE blocks.  Returns the number of items.
+  // Work items of a block range: COO groups (<= kGroupMembers consecutive COO blocks, nnz sum
+  // <= 32) and single CSR / DENSE / large-COO blocks.  Returns the number of items.
   auto count_items = [&](int64_t b0, int64_t b1) {
-    int64_t items = 0, lanes = 32;
+    int64_t items = 0, lanes = 32, members = 0;
     for (int64_t i = b0; i < b1; i++) {
       if (c.type[i] == CBSPMV_FMT_COO && c.nnzb[i] <= 32) {
-        if (lanes + c.nnzb[i] > 32) { items++; lanes = 0; }
+        if (lanes + c.nnzb[i] > 32 || members == kGroupMembers) { items++; lanes = 0; members = 0; }
         lanes += c.nnzb[i];
+        members++;
       } else {
         items++; lanes = 32;
       }
@@ -443,7 +444,7 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
     return items;
   };
   auto page_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
-    return kPageHeader + kDescBytes * (b1 - b0) + round_up(2 * count_items(b0, b1), 16) + rec_bytes;
+    return kPageHeader + kDescBytes * (b1 - b0) + round_up(4 * count_items(b0, b1), 16) + rec_bytes;
   };
   // x tile bytes per block gathered into the stage (non-aggregated matrices only; with aggregation
   // the consumer lanes gather x per element)
@@ -488,6 +489,7 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
   parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
     std::vector<uint32_t> w;
     std::vector<uint16_t> items;
+    std::vector<uint32_t> iwords;
     for (int64_t p = lo; p < hi; p++) {
       uint8_t *page = s->bytes + off[p];
       const int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
@@ -496,32 +498,42 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
       std::memset(page, 0, (size_t)(off[p + 1] - off[p]));
       // work items
       items.clear();
-      int64_t lanes = 32, head = -1;
+      iwords.clear();
+      int64_t lanes = 32, members = 0;
       for (int64_t i = b0; i < b1; i++) {
         const int64_t k = c.nnzb[i];
         if (c.type[i] == CBSPMV_FMT_COO && k <= 32) {
-          if (lanes + k > 32) { head = i; items.push_back((uint16_t)(i - b0)); lanes = 0; }
+          if (lanes + k > 32 || members == kGroupMembers) {
+            items.push_back((uint16_t)(i - b0));
+            iwords.push_back(item_word((uint32_t)(i - b0), CBSPMV_FMT_COO, 1, false));
+            lanes = 0; members = 0;
+          } else {  // another member of the current group: record its first lane
+            iwords.back() += 1u << 14;
+            iwords.back() |= (uint32_t)lanes << (16 + 5 * (members - 1));
+          }
           w[i - b0] = (uint32_t)lanes << 25;         // first lane of the block in its group
           lanes += k;
+          members++;
         } else {
-          head = i; items.push_back((uint16_t)(i - b0)); lanes = 32;
+          items.push_back((uint16_t)(i - b0));
+          iwords.push_back(item_word((uint32_t)(i - b0), (uint32_t)c.type[i], 1, c.type[i] == CBSPMV_FMT_COO));
+          lanes = 32;
           w[i - b0] = 0;
         }
-        (void)head;
       }
       const int64_t nitems = (int64_t)items.size();
       const int64_t item_off = kPageHeader + kDescBytes * nblk;
       const int64_t x_off = (int64_t)(off[p + 1] - off[p]);  // x tiles follow the page in its stage
       uint32_t hdr[4] = {(uint32_t)nblk, (uint32_t)nitems, (uint32_t)item_off, (uint32_t)x_off};
       std::memcpy(page, hdr, 16);
-      std::memcpy(page + item_off, items.data(), (size_t)nitems * 2);
+      std::memcpy(page + item_off, iwords.data(), (size_t)nitems * 4);
       // group sizes on the heads
       std::vector<uint32_t> gsize(nblk, 1);
       for (int64_t it = 0; it < nitems; it++) {
         const int64_t hb = items[it], he = it + 1 < nitems ? items[it + 1] : nblk;
         gsize[hb] = (uint32_t)(he - hb);
       }
-      int64_t pos = item_off + round_up(2 * nitems, 16);
+      int64_t pos = item_off + round_up(4 * nitems, 16);
       int64_t next_item = 0;
       for (int64_t i = b0; i < b1; i++) {
         const int64_t k = c.nnzb[i], S = c.val_size;

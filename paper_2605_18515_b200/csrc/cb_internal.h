@@ -13,7 +13,7 @@ namespace cb {
 // ---------------------------------------------------------------------------
 // Device page stream.  A derived layout of the canonical
 // format: blocks in slot order (after Alg. 2), whole thread blocks per page,
-//   page = header | desc[nblk] | item[nitems] (u16) | records
+//   page = header | desc[nblk] | item[nitems] (u32 words, see item_word) | records
 // every record 16-byte aligned and preceded by its block's restore_cols entries
 // when aggregated.  One cp.async.bulk moves a whole page into a
 // shared-memory stage; the page's x tiles (16 values per block, gathered on the
@@ -39,6 +39,15 @@ struct Desc {
                     // [25,30) first lane of the block within its COO group
 };
 constexpr uint32_t kFlagHead = 1u << 24;
+
+// Work-item word (page item table, one u32 per item):
+//   [0,12) head block index in the page; [12,14) type; [14,16) members - 1;
+//   [16,21), [21,26), [26,31) first lane of members 1, 2, 3 of a COO group;
+//   [31] a single COO block with nnz > 32 (processed in 32-element chunks)
+constexpr int kGroupMembers = 4;
+inline uint32_t item_word(uint32_t head, uint32_t type, uint32_t members, bool big) {
+  return head | (type << 12) | ((members - 1u) << 14) | (big ? 1u << 31 : 0u);
+}
 
 inline uint32_t pack_w(uint32_t nnz, uint32_t type, uint32_t ncols, bool head, uint32_t gsize, uint32_t lane0) {
   return (nnz - 1u) | (type << 8) | ((gsize - 1u) << 11) | (ncols << 16) | (head ? kFlagHead : 0u) | (lane0 << 25);

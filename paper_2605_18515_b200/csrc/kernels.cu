@@ -37,11 +37,11 @@
 
 namespace {
 
-constexpr int kGatherWarps = 4;
+constexpr int kGatherWarps = 4;    // x-tile gather warps (non-aggregated matrices only)
 constexpr int kGroupWarps = 6;     // consumer warps per group; a page is consumed by one group
-constexpr int kMaxGroups = 4;      // consumer groups per CTA (runtime: KParams::groups)
+constexpr int kMaxGroups = 5;      // consumer groups per CTA (runtime: KParams::groups)
 constexpr int kItemBatch = 1;      // work items claimed per consumer warp (2 measured slower on both workloads)
-constexpr int kMaxThreads = 32 * (1 + kGatherWarps + kMaxGroups * kGroupWarps);
+constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 16;
 constexpr int kSmemHeader = 512;  // mbarriers [3][16] + claims [16]; per-warp x scratch follows the ring
 constexpr unsigned kFull = 0xffffffffu;
@@ -181,14 +181,16 @@ struct CooPend {
 };
 
 template <typename V, bool AGG>
-__device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4 *descs, int hb, int gsize,
+__device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4 *descs, uint32_t iw,
                                                 const V *xbuf, const V *__restrict__ x, int lane, Dbg dbg) {
   CooPend<V> r;
-  const uint4 dj = descs[hb + min(lane, gsize - 1)];
-  const uint32_t starts = __reduce_or_sync(kFull, lane < gsize ? 1u << d_lane0(dj) : 0u);
-  const int mi = __popc(starts & ((2u << lane) - 1u)) - 1;
+  // group membership from the item word (first lanes of members 1..3; 0 = absent)
+  const int hb = iw & 0xFFF;
+  const int l1 = (iw >> 16) & 31, l2 = (iw >> 21) & 31, l3 = (iw >> 26) & 31;
+  const int mi = (l1 && lane >= l1) + (l2 && lane >= l2) + (l3 && lane >= l3);
+  const int lane0 = mi == 0 ? 0 : (mi == 1 ? l1 : (mi == 2 ? l2 : l3));
   const uint4 d = descs[hb + mi];
-  const int i = lane - d_lane0(d);
+  const int i = lane - lane0;
   r.valid = i < d_nnz(d);
   const uint8_t *body = page + (d.z & 0xFFFFu);
   const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&xready[s], P.tile_bulk ? 2 : 32 * kGatherWarps);
+      mbar_init(&xready[s], P.tile_bulk ? 2 : 32 * (AGG ? 1 : kGatherWarps));
       mbar_init(&empty[s], kGroupWarps);
       claim[s] = 0;
     }
@@ -361,8 +363,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     return;
   }
 
-  if (warp <= kGatherWarps) {
-    if constexpr (AGG) return;  // aggregated matrices: consumers gather x per element
+  constexpr int GW = AGG ? 0 : kGatherWarps;  // aggregated matrices: consumers gather x per element
+  if (warp <= GW) {
     // ---------------- gatherers: x tile of every block of the page -> shared
     const int gt = (warp - 1) * 32 + lane;
     int s = 0;
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   // issued before the current item is processed, hiding its latency)
   V scale = V(1);
   if constexpr (SCALED) scale = (V)(1.0 / sqrt(*P.sumsq));
-  const int cw = warp - 1 - kGatherWarps;
+  const int cw = warp - 1 - GW;
   V *wscratch = scratch + cw * 16;
   const int G = P.groups, grp = cw / kGroupWarps;
   int s = grp % S;
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
     const int nitems = (dbg.skip & 4) ? 0 : (int)hdr[1];
-    const uint16_t *items = reinterpret_cast<const uint16_t *>(page + hdr[2]);
+    const uint32_t *items = reinterpret_cast<const uint32_t *>(page + hdr[2]);
     const V *xbuf = reinterpret_cast<const V *>(page + hdr[3]);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
     // item pipeline: items are claimed kItemBatch at a time; the COO groups of a batch are
@@ -472,12 +474,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         nxt[j].valid = false;
         const int it = (int)k + j;
         if (it >= nitems) continue;
-        const int hb = items[it];
-        const uint4 dh = descs[hb];
-        const int t = d_type(dh);
-        if (t == CBSPMV_FMT_COO && d_nnz(dh) <= 32) {
-          nxt[j] = coo_issue<V, AGG>(page, descs, hb, d_gsize(dh), xbuf, x, lane, dbg);
+        const uint32_t iw = items[it];
+        const int t = (iw >> 12) & 3;
+        if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
+          nxt[j] = coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg);
         } else {
+          const int hb = iw & 0xFFF;
+          const uint4 dh = descs[hb];
           const V *xt = AGG ? warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg) : xbuf + hb * 16;
           if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
           else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
@@ -568,7 +571,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
   int ctas = env ? std::atoi(env) : 1;
   if (ctas < 1) ctas = 1;
   const char *genv = std::getenv("CBSPMV_GROUPS");
-  int groups = genv ? std::atoi(genv) : 4;
+  int groups = genv ? std::atoi(genv) : (dev->agg ? 5 : 4);
   groups = std::max(1, std::min(kMaxGroups, groups));
   dev->groups = groups;
   const int header = kSmemHeader + groups * kGroupWarps * 16 * (dev->dtype == CBSPMV_F64 ? 8 : 4);
@@ -620,7 +623,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * (dev.dtype == CBSPMV_F64 ? 8 : 4);
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
-    const int threads = 32 * (1 + kGatherWarps + dev.groups * kGroupWarps);
+    const int threads = 32 * (1 + (dev.agg ? 0 : kGatherWarps) + dev.groups * kGroupWarps);
     cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(threads), args, (size_t)smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "spmv kernel launch", err);
   }
