@@ -107,6 +107,9 @@ __device__ __forceinline__ void cp_async_elem(V *dst, const V *src) {
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src));
 }
+__device__ __forceinline__ void cp_async_16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src));
+}
 // Arrive on an mbarrier once all of this thread's prior cp.async copies have landed.
 __device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -311,6 +314,7 @@ struct KParams {
   int nstage;
   int groups;    // consumer groups in this CTA (page i of the CTA -> group i % groups)
   int tile_bulk; // non-aggregated x tiles: one cp.async.bulk per tile (x 16-byte aligned)
+  int vec16;     // non-aggregated x tiles: 16-byte cp.async (x 16-byte aligned)
   Dbg dbg;
 };
 
@@ -407,6 +411,34 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + reinterpret_cast<const uint32_t *>(page)[3]);
       const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
       constexpr int kG = 32 * kGatherWarps, kU = 4;
+      if (P.vec16) {
+        // non-aggregated, x 16-byte aligned: a tile is 16 contiguous values at bc*16, so each
+        // thread moves 16 bytes (kPer values) per cp.async; a partial last tile falls back to
+        // single values
+        constexpr int kPer = 16 / (int)sizeof(V), kChunks = 16 / kPer;
+        const int lim = (dbg.skip & 8) ? 0 : nblk * kChunks;
+        for (int t0 = gt; t0 < lim; t0 += kG * kU) {
+          uint4 d[kU];
+#pragma unroll
+          for (int j = 0; j < kU; j++) {
+            const int t = t0 + j * kG;
+            if (t < lim) d[j] = descs[t / kChunks];
+          }
+#pragma unroll
+          for (int j = 0; j < kU; j++) {
+            const int t = t0 + j * kG;
+            if (t >= lim) continue;
+            const int c = (t % kChunks) * kPer, nc = d_ncols(d[j]);
+            V *dst = xbuf + (t / kChunks) * 16 + c;
+            if (c + kPer <= nc) {
+              if (dbg.skip & 2) { for (int q = 0; q < kPer; q++) dst[q] = V(1); }
+              else cp_async_16(dst, x + d[j].y + c);
+            } else {
+              for (int q = c; q < nc; q++) cp_async_elem(xbuf + (t / kChunks) * 16 + q, x + d[j].y + q);
+            }
+          }
+        }
+      } else {
       const int lim = (dbg.skip & 8) ? 0 : nblk * 16;
       for (int t0 = gt; t0 < lim; t0 += kG * kU) {
         uint32_t col[kU];
@@ -431,6 +463,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             else cp_async_elem(dst, x + col[j]);
           }
         }
+      }
       }
       cp_async_arrive(&xready[s]);
       if (++s == S) { s = 0; parity ^= 1u; }
@@ -618,8 +651,9 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     // page copies in the TMA engine); kept behind CBSPMV_TILE_BULK=1 for experiments.
     static const int bulk_env = [] { const char *v = std::getenv("CBSPMV_TILE_BULK"); return v ? std::atoi(v) : 0; }();
     const int tile_bulk = bulk_env && !dev.agg && ((uintptr_t)x % 16 == 0);
+    const int vec16 = !dev.agg && ((uintptr_t)x % 16 == 0);
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, dev.groups, tile_bulk,
-              Dbg{dbg_skip}};
+              vec16, Dbg{dbg_skip}};
     const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * (dev.dtype == CBSPMV_F64 ? 8 : 4);
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
