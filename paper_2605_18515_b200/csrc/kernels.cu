@@ -100,15 +100,33 @@ __device__ __forceinline__ void mbar_tx_complete_local(uint64_t *bar, uint32_t b
 }
 // Asynchronous gather of one x value into shared memory (SASS LDGSTS).
 template <typename V>
-__device__ __forceinline__ void cp_async_elem(V *dst, const V *src) {
+__device__ __forceinline__ void cp_async_elem(V *dst, const V *src, uint64_t pol) {
   // no "memory" clobber: the destination is read only after the xready mbarrier wait
   if constexpr (sizeof(V) == 8)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src));
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
   else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src));
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
 }
-__device__ __forceinline__ void cp_async_16(void *dst, const void *src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src));
+__device__ __forceinline__ void cp_async_16(void *dst, const void *src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+               "l"(pol));
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// x gathered straight into a register, L2 evict_last (x is re-read; the matrix stream is evict_first)
+template <typename V>
+__device__ __forceinline__ V ldg_x(const V *p, uint64_t pol) {
+  V v;
+  if constexpr (sizeof(V) == 8)
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  else
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
 }
 // Arrive on an mbarrier once all of this thread's prior cp.async copies have landed.
 __device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
@@ -185,7 +203,8 @@ struct CooPend {
 
 template <typename V, bool AGG>
 __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4 *descs, uint32_t iw,
-                                                const V *xbuf, const V *__restrict__ x, int lane, Dbg dbg) {
+                                                const V *xbuf, const V *__restrict__ x, int lane, Dbg dbg,
+                                                uint64_t xpol) {
   CooPend<V> r;
   // group membership from the item word (first lanes of members 1..3; 0 = absent)
   const int hb = iw & 0xFFF;
@@ -205,7 +224,7 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   if (r.valid) {
     if constexpr (AGG) {
       const uint32_t c = reinterpret_cast<const uint32_t *>(page + d.y)[col];
-      r.xv = (dbg.skip & 2) ? V(1) + V(c & 1) : __ldg(x + c);
+      r.xv = (dbg.skip & 2) ? V(1) + V(c & 1) : ldg_x(x + c, xpol);
     } else {
       r.xv = xbuf[(hb + mi) * 16 + col];
     }
@@ -371,6 +390,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   if (warp <= GW) {
     // ---------------- gatherers: x tile of every block of the page -> shared
     const int gt = (warp - 1) * 32 + lane;
+    const uint64_t xpol = policy_evict_last();
     int s = 0;
     uint32_t parity = 0;
     if (P.tile_bulk) {
@@ -432,9 +452,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             V *dst = xbuf + (t / kChunks) * 16 + c;
             if (c + kPer <= nc) {
               if (dbg.skip & 2) { for (int q = 0; q < kPer; q++) dst[q] = V(1); }
-              else cp_async_16(dst, x + d[j].y + c);
+              else cp_async_16(dst, x + d[j].y + c, xpol);
             } else {
-              for (int q = c; q < nc; q++) cp_async_elem(xbuf + (t / kChunks) * 16 + q, x + d[j].y + q);
+              for (int q = c; q < nc; q++) cp_async_elem(xbuf + (t / kChunks) * 16 + q, x + d[j].y + q, xpol);
             }
           }
         }
@@ -460,7 +480,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
           if (ok[j]) {
             V *dst = xbuf + t0 + j * kG;
             if (dbg.skip & 2) *dst = V(1) + V(col[j] & 1);
-            else cp_async_elem(dst, x + col[j]);
+            else cp_async_elem(dst, x + col[j], xpol);
           }
         }
       }
@@ -477,6 +497,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   if constexpr (SCALED) scale = (V)(1.0 / sqrt(*P.sumsq));
   const int cw = warp - 1 - GW;
   V *wscratch = scratch + cw * 16;
+  const uint64_t xpolc = policy_evict_last();
   const int G = P.groups, grp = cw / kGroupWarps;
   int s = grp % S;
   uint32_t parity = (uint32_t)((grp / S) & 1);
@@ -510,7 +531,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         const uint32_t iw = items[it];
         const int t = (iw >> 12) & 3;
         if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
-          nxt[j] = coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg);
+          nxt[j] = coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpolc);
         } else {
           const int hb = iw & 0xFFF;
           const uint4 dh = descs[hb];
