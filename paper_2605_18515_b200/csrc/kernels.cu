@@ -1,30 +1,26 @@
 // kernels.cu — sm_100a kernels of the CB-SpMV hot path (y = A·x, §3.5).
 //
-// One persistent CTA per SM streams its contiguous range of device pages
-// through a ring of shared-memory stages:
-//   warp 0 (one elected lane)  : producer — mbarrier wait on "empty", then one
-//                                cp.async.bulk (TMA, SASS UBLKCP) per page into the stage,
-//                                completion counted on the stage's "full" mbarrier;
-//                                pages are streamed with an L2 evict_first policy so the
-//                                matrix does not evict x.
-//   warps 1..kConsumerWarps    : consumers — each takes blocks of the page, one block per
-//                                warp at a time (the paper's warp <-> sub-block mapping,
-//                                P:403), U blocks batched so their x gathers overlap.
-// Per-format warp paths (one warp per sub-block):
-//   COO   (Alg. 3): lane i <-> element i; coordinate byte row = b & 15,
-//         col = b >> 4; x from the 16-lane x tile by shuffle; products
-//         reduced per row with a segmented warp shuffle, one RED per distinct row
-//         instead of one atomic per element.
-//   CSR   ("optimizing intra-block computation using the shfl function",
-//         P:570 "32 threads collaboratively compute 16 y elements"): two lanes per row.
-//   DENSE (Alg. 4): 256 row-major values, conflict-free 8-byte shared loads,
-//         a transposing xor-butterfly (8,4,2,1) leaves one full row sum per lane pair.
-// x tile: lane l holds x for column (l & 15) of the block —
-//   x[bc*16 + c] without aggregation (replaces the shared-memory s_x), or
-//   x[restore_cols[cols_offset[br] + bc*16 + c]] with aggregation (the restore entries
-//   are inlined in front of the record in the page).
-// y is accumulated with red.global.add (atomicAdd without return), as the paper's
-// atomicAdd; y is zeroed first by cb_zero_kernel (R-16).
+// One persistent CTA per SM streams its contiguous range of device pages (DESIGN.md §4)
+// through a ring of 28 KB shared-memory stages (8 stages):
+//   warp 0 (one elected lane): TMA producer — waits on the stage's "empty" mbarrier, then one
+//       cp.async.bulk (SASS UBLKCP) per page, L2 evict_first (the stream must not evict x);
+//       completion counted on the stage's "full" mbarrier.
+//   5 consumer groups x 6 warps: page i of the CTA goes to group i % 5; the group's warps claim
+//       the page's work items from a shared counter:
+//       * COO group (Alg. 3): up to 4 consecutive COO blocks packed into one warp,
+//         lane <-> element, coordinate byte row = b & 15, col = b >> 4, one RED
+//         per element — Alg. 3's atomicAdd — issued as one warp instruction per group;
+//       * CSR ("32 threads collaboratively compute 16 y elements"): two lanes
+//         per row, one shfl_xor;
+//       * DENSE (Alg. 4): lane-major device layout, 8 FMAs per lane, one
+//         shfl_xor(16) (R-15 semantics), 16 REDs.
+// x: without aggregation each item's 16-value tiles x[bc*16 ..] are copied
+// into the stage with 16-byte cp.async one item ahead of processing (replaces the paper's
+// shared-memory s_x preload); with aggregation each lane gathers
+// x[restore_cols[cols_offset[br] + bc*16 + col]] straight into a register, the next COO
+// group's loads issued before the current one is finished.  The restore entries travel in
+// front of each block's record.  y is zeroed by cb_zero_kernel (R-16) and accumulated with
+// red.global.add (the paper's atomicAdd).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -37,13 +33,12 @@
 
 namespace {
 
-constexpr int kGatherWarps = 4;    // x-tile gather warps (non-aggregated matrices only)
 constexpr int kGroupWarps = 6;     // consumer warps per group; a page is consumed by one group
 constexpr int kMaxGroups = 5;      // consumer groups per CTA (runtime: KParams::groups)
 constexpr int kItemBatch = 1;      // work items claimed per consumer warp (2 measured slower on both workloads)
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 16;
-constexpr int kSmemHeader = 512;  // mbarriers [3][16] + claims [16]; per-warp x scratch follows the ring
+constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16]; warp scratch follows the ring
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -89,26 +84,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s_nohint(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_tx_complete_local(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-// Asynchronous gather of one x value into shared memory (SASS LDGSTS).
-template <typename V>
-__device__ __forceinline__ void cp_async_elem(V *dst, const V *src, uint64_t pol) {
-  // no "memory" clobber: the destination is read only after the xready mbarrier wait
-  if constexpr (sizeof(V) == 8)
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
-                 "l"(pol));
-  else
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src),
-                 "l"(pol));
-}
 __device__ __forceinline__ void cp_async_16(void *dst, const void *src, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
                "l"(pol));
@@ -127,10 +102,6 @@ __device__ __forceinline__ V ldg_x(const V *p, uint64_t pol) {
   else
     asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   return v;
-}
-// Arrive on an mbarrier once all of this thread's prior cp.async copies have landed.
-__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
 // Ablation knob for profiling only (env CBSPMV_DEBUG_SKIP, a kernel argument held in a
@@ -332,19 +303,42 @@ struct KParams {
   int stage;     // bytes per stage: page data + its x tiles
   int nstage;
   int groups;    // consumer groups in this CTA (page i of the CTA -> group i % groups)
-  int tile_bulk; // non-aggregated x tiles: one cp.async.bulk per tile (x 16-byte aligned)
   int vec16;     // non-aggregated x tiles: 16-byte cp.async (x 16-byte aligned)
   Dbg dbg;
 };
 
-// Warp roles: 0 = TMA producer, 1..kGatherWarps = x gatherers, the rest = consumers.
+// Issue the x tiles of a work item's blocks (non-aggregated: x[bc*16 .. bc*16 + ncols)) into
+// their slots of the stage's tile area with 16-byte cp.async (8 lanes per fp64 tile, up to 4
+// member blocks per item), as one cp.async group; used one item ahead of processing.
+template <typename V>
+__device__ __forceinline__ void issue_tiles(const uint4 *descs, uint32_t iw, V *xbuf, const V *__restrict__ x,
+                                            bool vec16, uint64_t pol, int lane, Dbg dbg) {
+  constexpr int kPer = 16 / (int)sizeof(V), kChunks = 16 / kPer;
+  const int hb = iw & 0xFFF;
+  const int members = (int)((iw >> 14) & 3) + 1;
+  const int mem = lane / kChunks, c = (lane % kChunks) * kPer;
+  if (mem < members && !(dbg.skip & 8)) {
+    const uint4 d = descs[hb + mem];
+    const int nc = d_ncols(d);
+    V *dst = xbuf + (hb + mem) * 16 + c;
+    if (dbg.skip & 2) {
+      for (int q = 0; q < kPer; q++) dst[q] = V(1);
+    } else if (vec16 && c + kPer <= nc) {
+      cp_async_16(dst, x + d.y + c, pol);
+    } else {
+      for (int q = c; q < c + kPer && q < nc; q++) cp_async_elem(dst + (q - c), x + d.y + q, pol);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Warp roles: 0 = TMA producer, the rest = consumer groups.
 template <typename V, bool AGG, bool SCALED>
 __global__ void __launch_bounds__(kMaxThreads, 1)
     cb_spmv_kernel(KParams P, const V *__restrict__ x, V *__restrict__ y) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-  uint64_t *xready = full + kMaxStages;
-  uint64_t *empty = xready + kMaxStages;
+  uint64_t *empty = full + 2 * kMaxStages;
   uint32_t *claim = reinterpret_cast<uint32_t *>(empty + kMaxStages);
   uint8_t *ring = smem + kSmemHeader;
   V *scratch = reinterpret_cast<V *>(ring + (size_t)P.nstage * P.stage);  // 16 values per consumer warp
@@ -357,7 +351,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&xready[s], P.tile_bulk ? 2 : 32 * (AGG ? 1 : kGatherWarps));
       mbar_init(&empty[s], kGroupWarps);
       claim[s] = 0;
     }
@@ -386,171 +379,82 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     return;
   }
 
-  constexpr int GW = AGG ? 0 : kGatherWarps;  // aggregated matrices: consumers gather x per element
-  if (warp <= GW) {
-    // ---------------- gatherers: x tile of every block of the page -> shared
-    const int gt = (warp - 1) * 32 + lane;
-    const uint64_t xpol = policy_evict_last();
-    int s = 0;
-    uint32_t parity = 0;
-    if (P.tile_bulk) {
-      // non-aggregated: tile = x[bc*16 .. bc*16 + ncols) is contiguous -> one TMA bulk copy per
-      // block (16-byte multiple), the odd tail (if any) by a plain load; gather warp 0 only.
-      if (warp != 1) return;
-      for (uint32_t p = p0; p < p1; p++) {
-        mbar_wait(&full[s], parity);
-        const uint8_t *page = ring + (size_t)s * P.stage;
-        const int nblk = *reinterpret_cast<const uint32_t *>(page);
-        V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + reinterpret_cast<const uint32_t *>(page)[3]);
-        const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
-        constexpr int kPer16 = 16 / (int)sizeof(V);  // values per 16 bytes
-        uint32_t bytes = 0;
-        for (int b = lane; b < nblk; b += 32) bytes += (uint32_t)(d_ncols(descs[b]) / kPer16 * 16);
-        bytes = __reduce_add_sync(kFull, bytes);
-        if (lane == 0) mbar_arrive_expect_tx(&xready[s], bytes);
-        __syncwarp();
-        for (int b = lane; b < nblk; b += 32) {
-          const uint4 d = descs[b];
-          const int nc = d_ncols(d), nbulk = nc / kPer16 * kPer16;
-          if (nbulk > 0) {
-            if (dbg.skip & 2) { for (int c = 0; c < nbulk; c++) xbuf[b * 16 + c] = V(1); mbar_tx_complete_local(&xready[s], nbulk * sizeof(V)); }
-            else bulk_g2s_nohint(xbuf + b * 16, x + d.y, (uint32_t)(nbulk * sizeof(V)), &xready[s]);
-          }
-          for (int c = nbulk; c < nc; c++) xbuf[b * 16 + c] = __ldg(x + d.y + c);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&xready[s]);
-        if (++s == S) { s = 0; parity ^= 1u; }
-      }
-      return;
-    }
-    for (uint32_t p = p0; p < p1; p++) {
-      mbar_wait(&full[s], parity);
-      const uint8_t *page = ring + (size_t)s * P.stage;
-      const int nblk = *reinterpret_cast<const uint32_t *>(page);
-      V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + reinterpret_cast<const uint32_t *>(page)[3]);
-      const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
-      constexpr int kG = 32 * kGatherWarps, kU = 4;
-      if (P.vec16) {
-        // non-aggregated, x 16-byte aligned: a tile is 16 contiguous values at bc*16, so each
-        // thread moves 16 bytes (kPer values) per cp.async; a partial last tile falls back to
-        // single values
-        constexpr int kPer = 16 / (int)sizeof(V), kChunks = 16 / kPer;
-        const int lim = (dbg.skip & 8) ? 0 : nblk * kChunks;
-        for (int t0 = gt; t0 < lim; t0 += kG * kU) {
-          uint4 d[kU];
-#pragma unroll
-          for (int j = 0; j < kU; j++) {
-            const int t = t0 + j * kG;
-            if (t < lim) d[j] = descs[t / kChunks];
-          }
-#pragma unroll
-          for (int j = 0; j < kU; j++) {
-            const int t = t0 + j * kG;
-            if (t >= lim) continue;
-            const int c = (t % kChunks) * kPer, nc = d_ncols(d[j]);
-            V *dst = xbuf + (t / kChunks) * 16 + c;
-            if (c + kPer <= nc) {
-              if (dbg.skip & 2) { for (int q = 0; q < kPer; q++) dst[q] = V(1); }
-              else cp_async_16(dst, x + d[j].y + c, xpol);
-            } else {
-              for (int q = c; q < nc; q++) cp_async_elem(xbuf + (t / kChunks) * 16 + q, x + d[j].y + q, xpol);
-            }
-          }
-        }
-      } else {
-      const int lim = (dbg.skip & 8) ? 0 : nblk * 16;
-      for (int t0 = gt; t0 < lim; t0 += kG * kU) {
-        uint32_t col[kU];
-        bool ok[kU];
-#pragma unroll
-        for (int j = 0; j < kU; j++) {  // independent: descriptor + restore loads of kU tiles first
-          const int t = t0 + j * kG;
-          ok[j] = false;
-          col[j] = 0;
-          if (t < lim) {
-            const uint4 d = descs[t >> 4];
-            const int c = t & 15;
-            ok[j] = c < d_ncols(d);
-            if (ok[j]) col[j] = AGG ? reinterpret_cast<const uint32_t *>(page + d.y)[c] : d.y + c;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kU; j++) {
-          if (ok[j]) {
-            V *dst = xbuf + t0 + j * kG;
-            if (dbg.skip & 2) *dst = V(1) + V(col[j] & 1);
-            else cp_async_elem(dst, x + col[j], xpol);
-          }
-        }
-      }
-      }
-      cp_async_arrive(&xready[s]);
-      if (++s == S) { s = 0; parity ^= 1u; }
-    }
-    return;
-  }
-
-  // ---------------- consumers: claim the page's work items one at a time (the next claim is
-  // issued before the current item is processed, hiding its latency)
+  // ---------------- consumers: group g takes pages g, g + G, ...; its warps claim work items.
+  // Aggregated matrices gather x per element straight into registers (the next COO group's
+  // loads are issued before the current one is finished); non-aggregated matrices copy each
+  // item's x tiles into the stage one item ahead (cp.async groups).
   V scale = V(1);
   if constexpr (SCALED) scale = (V)(1.0 / sqrt(*P.sumsq));
-  const int cw = warp - 1 - GW;
+  const int cw = warp - 1;
   V *wscratch = scratch + cw * 16;
-  const uint64_t xpolc = policy_evict_last();
+  const uint64_t xpol = policy_evict_last();
   const int G = P.groups, grp = cw / kGroupWarps;
   int s = grp % S;
   uint32_t parity = (uint32_t)((grp / S) & 1);
   for (uint32_t p = p0 + grp; p < p1; p += G) {
     mbar_wait(&full[s], parity);
-    if constexpr (!AGG) mbar_wait(&xready[s], parity);
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
     const int nitems = (dbg.skip & 4) ? 0 : (int)hdr[1];
     const uint32_t *items = reinterpret_cast<const uint32_t *>(page + hdr[2]);
-    const V *xbuf = reinterpret_cast<const V *>(page + hdr[3]);
+    V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + hdr[3]);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
-    // item pipeline: items are claimed kItemBatch at a time; the COO groups of a batch are
-    // issued (all loads, including the x gathers, in flight) before the previous batch is
-    // finished (multiply + RED); CSR / DENSE items run synchronously
-    CooPend<V> pend[kItemBatch];
-#pragma unroll
-    for (int j = 0; j < kItemBatch; j++) pend[j].valid = false;
     uint32_t k = 0;
-    if (lane == 0) k = atomicAdd(&claim[s], (uint32_t)kItemBatch);
+    if (lane == 0) k = atomicAdd(&claim[s], 1u);
     k = __shfl_sync(kFull, k, 0);
-    while ((int)k < nitems) {
-      uint32_t kn = 0;
-      if (lane == 0) kn = atomicAdd(&claim[s], (uint32_t)kItemBatch);
-      CooPend<V> nxt[kItemBatch];
-#pragma unroll
-      for (int j = 0; j < kItemBatch; j++) {
-        nxt[j].valid = false;
-        const int it = (int)k + j;
-        if (it >= nitems) continue;
-        const uint32_t iw = items[it];
+    if constexpr (AGG) {
+      CooPend<V> pend;
+      pend.valid = false;
+      while ((int)k < nitems) {
+        uint32_t kn = 0;
+        if (lane == 0) kn = atomicAdd(&claim[s], 1u);
+        const uint32_t iw = items[k];
         const int t = (iw >> 12) & 3;
+        CooPend<V> nxt;
+        nxt.valid = false;
         if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
-          nxt[j] = coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpolc);
+          nxt = coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol);
         } else {
-          const int hb = iw & 0xFFF;
-          const uint4 dh = descs[hb];
-          const V *xt = AGG ? warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg) : xbuf + hb * 16;
+          const uint4 dh = descs[iw & 0xFFF];
+          const V *xt = warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg);
           if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
           else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
           else dense_path<V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
           __syncwarp();
         }
+        coo_finish<V, SCALED>(pend, scale, y, dbg);
+        pend = nxt;
+        k = __shfl_sync(kFull, kn, 0);
       }
-#pragma unroll
-      for (int j = 0; j < kItemBatch; j++) {
-        coo_finish<V, SCALED>(pend[j], scale, y, dbg);
-        pend[j] = nxt[j];
+      coo_finish<V, SCALED>(pend, scale, y, dbg);
+    } else {
+      uint32_t iw = (int)k < nitems ? items[k] : 0u;
+      if ((int)k < nitems) issue_tiles<V>(descs, iw, xbuf, x, P.vec16, xpol, lane, dbg);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      while ((int)k < nitems) {
+        uint32_t kn = 0;
+        if (lane == 0) kn = atomicAdd(&claim[s], 1u);
+        kn = __shfl_sync(kFull, kn, 0);
+        const uint32_t iwn = (int)kn < nitems ? items[kn] : 0u;
+        if ((int)kn < nitems) issue_tiles<V>(descs, iwn, xbuf, x, P.vec16, xpol, lane, dbg);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // item k's tiles have landed
+        __syncwarp();
+        const int t = (iw >> 12) & 3, hb = iw & 0xFFF;
+        if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
+          coo_finish<V, SCALED>(coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
+        } else {
+          const uint4 dh = descs[hb];
+          const V *xt = xbuf + hb * 16;
+          if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+          else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+          else dense_path<V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
+        }
+        k = kn;
+        iw = iwn;
       }
-      k = __shfl_sync(kFull, kn, 0);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-#pragma unroll
-    for (int j = 0; j < kItemBatch; j++) coo_finish<V, SCALED>(pend[j], scale, y, dbg);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     s += G;
@@ -625,7 +529,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
   int ctas = env ? std::atoi(env) : 1;
   if (ctas < 1) ctas = 1;
   const char *genv = std::getenv("CBSPMV_GROUPS");
-  int groups = genv ? std::atoi(genv) : (dev->agg ? 5 : 4);
+  int groups = genv ? std::atoi(genv) : 5;
   groups = std::max(1, std::min(kMaxGroups, groups));
   dev->groups = groups;
   const int header = kSmemHeader + groups * kGroupWarps * 16 * (dev->dtype == CBSPMV_F64 ? 8 : 4);
@@ -668,17 +572,13 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
   }();
   if (dev.n_pages > 0) {
     const int stage = dev.page_cap;
-    // TMA-bulk x tiles measured slower than LDGSTS on B200 (the small tile copies queue behind the
-    // page copies in the TMA engine); kept behind CBSPMV_TILE_BULK=1 for experiments.
-    static const int bulk_env = [] { const char *v = std::getenv("CBSPMV_TILE_BULK"); return v ? std::atoi(v) : 0; }();
-    const int tile_bulk = bulk_env && !dev.agg && ((uintptr_t)x % 16 == 0);
     const int vec16 = !dev.agg && ((uintptr_t)x % 16 == 0);
-    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, dev.groups, tile_bulk,
+    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, dev.groups,
               vec16, Dbg{dbg_skip}};
     const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * (dev.dtype == CBSPMV_F64 ? 8 : 4);
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
-    const int threads = 32 * (1 + (dev.agg ? 0 : kGatherWarps) + dev.groups * kGroupWarps);
+    const int threads = 32 * (1 + dev.groups * kGroupWarps);
     cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(threads), args, (size_t)smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "spmv kernel launch", err);
   }
