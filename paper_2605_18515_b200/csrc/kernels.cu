@@ -84,6 +84,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
       : "memory");
 }
+// Asynchronous copy of one x value into shared memory (SASS LDGSTS).
+template <typename V>
+__device__ __forceinline__ void cp_async_elem(V *dst, const V *src, uint64_t pol) {
+  // no "memory" clobber: the destination is read only after cp.async.wait_group + __syncwarp
+  if constexpr (sizeof(V) == 8)
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
+  else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
+}
 __device__ __forceinline__ void cp_async_16(void *dst, const void *src, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
                "l"(pol));
