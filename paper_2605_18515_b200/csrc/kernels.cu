@@ -410,35 +410,52 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const uint32_t *items = reinterpret_cast<const uint32_t *>(page + hdr[2]);
     V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + hdr[3]);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
-    uint32_t k = 0;
-    if (lane == 0) k = atomicAdd(&claim[s], 1u);
-    k = __shfl_sync(kFull, k, 0);
     if constexpr (AGG) {
-      CooPend<V> pend;
-      pend.valid = false;
-      while ((int)k < nitems) {
+      // Claims of 4 items.  When all 4 are COO groups (the common case on aggregated, super-
+      // sparse matrices) their load chains (descriptor -> record -> restore entry -> x) are
+      // issued straight-line so the four chains overlap, then the four are finished.
+      uint32_t kb = 0;
+      if (lane == 0) kb = atomicAdd(&claim[s], 4u);
+      kb = __shfl_sync(kFull, kb, 0);
+      // the claim counter starts at 0 and moves by 4: kb is a multiple of 4 (16-byte aligned), and
+      // the item table is zero-padded to 16 bytes, so the 128-bit load stays inside the page
+      while ((int)kb < nitems) {
         uint32_t kn = 0;
-        if (lane == 0) kn = atomicAdd(&claim[s], 1u);
-        const uint32_t iw = items[k];
-        const int t = (iw >> 12) & 3;
-        CooPend<V> nxt;
-        nxt.valid = false;
-        if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
-          nxt = coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol);
+        if (lane == 0) kn = atomicAdd(&claim[s], 4u);
+        const uint4 iw4 = *reinterpret_cast<const uint4 *>(items + kb);
+        const uint32_t iws[4] = {iw4.x, iw4.y, iw4.z, iw4.w};
+        const int nv = min(4, nitems - (int)kb);
+        bool all_coo = nv == 4;
+#pragma unroll
+        for (int j = 0; j < 4; j++) all_coo &= ((iws[j] >> 12) & 3) == CBSPMV_FMT_COO && !(iws[j] >> 31);
+        if (all_coo) {
+          CooPend<V> q[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) q[j] = coo_issue<V, AGG>(page, descs, iws[j], xbuf, x, lane, dbg, xpol);
+#pragma unroll
+          for (int j = 0; j < 4; j++) coo_finish<V, SCALED>(q[j], scale, y, dbg);
         } else {
-          const uint4 dh = descs[iw & 0xFFF];
-          const V *xt = warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg);
-          if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
-          else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
-          else dense_path<V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
-          __syncwarp();
+          for (int j = 0; j < nv; j++) {
+            const uint32_t iw = iws[j];
+            const int t = (iw >> 12) & 3;
+            if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
+              coo_finish<V, SCALED>(coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
+            } else {
+              const uint4 dh = descs[iw & 0xFFF];
+              const V *xt = warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg);
+              if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+              else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+              else dense_path<V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
+              __syncwarp();
+            }
+          }
         }
-        coo_finish<V, SCALED>(pend, scale, y, dbg);
-        pend = nxt;
-        k = __shfl_sync(kFull, kn, 0);
+        kb = __shfl_sync(kFull, kn, 0);
       }
-      coo_finish<V, SCALED>(pend, scale, y, dbg);
     } else {
+      uint32_t k = 0;
+      if (lane == 0) k = atomicAdd(&claim[s], 1u);
+      k = __shfl_sync(kFull, k, 0);
       uint32_t iw = (int)k < nitems ? items[k] : 0u;
       if ((int)k < nitems) issue_tiles<V>(descs, iw, xbuf, x, P.vec16, xpol, lane, dbg);
       else asm volatile("cp.async.commit_group;" ::: "memory");

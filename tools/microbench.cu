@@ -204,5 +204,16 @@ int main() {
     run(nm, [&] { k_red_act<<<blocks, threads>>>(y, n, iters, act); }, warp_instr);
   }
   run("LDS.64 consecutive (dependent chain)", [&] { k_lds<<<blocks, threads>>>(out, iters); }, warp_instr);
+  // is the RED cost per SM or chip-wide?  same work per warp on half / quarter of the SMs
+  for (int frac : {2, 4}) {
+    char nm[128];
+    snprintf(nm, sizeof nm, "RED f64 16 lanes 1 line, grid/%d", frac);
+    const int b = blocks / frac;
+    double instr = (double)b * threads / 32 * iters;
+    run(nm, [&] { k_red_act<<<b, threads>>>(y, n, iters, 16); }, instr);
+  }
+  // RED + scattered LDG in the same warp loop
+  run("LDG scattered + RED f64 (1 line), per pair", [&] { k_gather<0><<<blocks, threads>>>(x, n, iters, out, 0);
+      k_red_act<<<blocks, threads>>>(y, n, iters, 16); }, warp_instr);
   return 0;
 }
