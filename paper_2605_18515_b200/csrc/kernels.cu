@@ -285,7 +285,10 @@ __device__ __forceinline__ void dense_path(const uint8_t *page, const uint4 &d, 
   // absent entries (stored zeros) must contribute 0 even against non-finite x: check the tile once
   const bool finite = __all_sync(kFull, r >= nc || isfinite(xt[r]));
   V acc = V(0);
-  if (finite) {
+  if (finite && nc == 16) {  // full tile (every block column but a ragged last one)
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc = fma(vals[k * 32 + lane], xt[h * 8 + k], acc);
+  } else if (finite) {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const int c = h * 8 + k;
