@@ -35,7 +35,6 @@ namespace {
 
 constexpr int kGroupWarps = 6;     // consumer warps per group; a page is consumed by one group
 constexpr int kMaxGroups = 5;      // consumer groups per CTA (runtime: KParams::groups)
-constexpr int kItemBatch = 1;      // work items claimed per consumer warp (2 measured slower on both workloads)
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 16;
 constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16]; warp scratch follows the ring
@@ -134,48 +133,17 @@ __device__ __forceinline__ void red_add(V *p, V v, Dbg dbg) {
 __device__ __forceinline__ int d_type(const uint4 &d) { return (d.w >> 8) & 3; }
 __device__ __forceinline__ int d_nnz(const uint4 &d) { return (int)(d.w & 0xFF) + 1; }
 __device__ __forceinline__ int d_ncols(const uint4 &d) { return (d.w >> 16) & 31; }
-__device__ __forceinline__ int d_gsize(const uint4 &d) { return (int)((d.w >> 11) & 31) + 1; }
-__device__ __forceinline__ int d_lane0(const uint4 &d) { return (int)((d.w >> 25) & 31); }
 
 // ------------------------------------------------------------------ per-format warp paths
-// xt: the block's 16-value x tile in shared memory (filled by the gather warps):
+// xt: the block's 16-value x tile in shared memory (copied one work item ahead):
 //   x[bc*16 + c] without aggregation (the paper's shared-memory s_x), or
 //   x[restore_cols[cols_offset[br] + bc*16 + c]] with aggregation.
 
-// COO group (Alg. 3): consecutive COO blocks packed into one warp, lane <-> element; the
-// coordinate byte gives row = b & 15, col = b >> 4; one RED per element into y,
-// Alg. 3's atomicAdd, issued as one warp instruction.
-template <typename V, bool AGG, bool SCALED>
-__device__ __forceinline__ void coo_group(const uint8_t *page, const uint4 *descs, int hb, int gsize,
-                                          const V *xbuf, const V *__restrict__ x, V scale, V *__restrict__ y,
-                                          int lane, Dbg dbg) {
-  const uint4 dj = descs[hb + min(lane, gsize - 1)];
-  const uint32_t starts = __reduce_or_sync(kFull, lane < gsize ? 1u << d_lane0(dj) : 0u);
-  const int mi = __popc(starts & ((2u << lane) - 1u)) - 1;  // member block of this lane
-  const uint4 d = descs[hb + mi];
-  const int i = lane - d_lane0(d);
-  const bool valid = i < d_nnz(d);
-  const uint8_t *body = page + (d.z & 0xFFFFu);
-  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
-  const uint32_t byte = valid ? body[i] : 0u;
-  const int row = byte & 15, col = byte >> 4;
-  if (valid) {
-    V xv;
-    if constexpr (AGG) {  // x[restore_cols[cols_offset[br] + bc*16 + col]], straight to a register
-      const uint32_t c = reinterpret_cast<const uint32_t *>(page + d.y)[col];
-      xv = (dbg.skip & 2) ? V(1) + V(c & 1) : __ldg(x + c);
-    } else {
-      xv = xbuf[(hb + mi) * 16 + col];
-    }
-    V p = vals[i] * xv;
-    if constexpr (SCALED) p *= scale;
-    red_add(y + d.x + row, p, dbg);
-  }
-}
-
-// Split-phase COO group for software pipelining: issue() performs every load (descriptors,
-// element, and the x gather) and finish() multiplies and issues the RED, so a warp keeps the x
-// gathers of two work items in flight.
+// COO group (Alg. 3): up to 4 consecutive COO blocks packed into one warp, lane <-> element;
+// the coordinate byte gives row = b & 15, col = b >> 4; one RED per element into y
+// (Alg. 3's atomicAdd), issued as one warp instruction.  Split in two phases:
+// coo_issue() performs every load (descriptor, element, restore entry, x) and coo_finish()
+// multiplies and issues the RED, so several groups' loads can be in flight together.
 template <typename V>
 struct CooPend {
   V v, xv;

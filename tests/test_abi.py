@@ -59,3 +59,16 @@ def test_host_only_handle_refuses_device_calls():
     assert h.info["nb"] == 1
     cb.destroy(h)
     np.testing.assert_equal(h._raw, None)
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    """No fallback: without libcbspmv.so every entry point raises."""
+    import pytest
+    mod = cb
+    monkeypatch.setattr(mod, "LIB_PATH", str(tmp_path / "nope.so"))
+    monkeypatch.setattr(mod, "_lib", None)
+    with pytest.raises(RuntimeError):
+        mod.lib()
+    import synth
+    with pytest.raises(RuntimeError):
+        mod.build(synth.fig1(), device=-1)

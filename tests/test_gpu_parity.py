@@ -247,18 +247,6 @@ def test_device_stream_encodes_canonical_format(name):
         assert np.array_equal(dev_rec, ex["mtx_data"][vp:vp + size])
 
 
-@pytest.mark.parametrize("segred", ["0", "1"])
-def test_coo_reduction_modes(segred, monkeypatch):
-    """Both COO accumulation modes (RED per element / segmented reduction) match the oracle."""
-    monkeypatch.setenv("CBSPMV_COO_SEGRED", segred)
-    for A in (synth.make("rmat", small=True), synth.random_csr(300, 300, 0.05, 3, pattern="hub")):
-        x = synth.vector(A.n, synth.VEC_UNIFORM, seed=2)
-        y_ref, R = oracle.spmv_csr(A, x)
-        for ff in (-1, 0):
-            y, _ = gpu_spmv(A, x, force_format=ff)
-            check_rows(y, y_ref, R, 1e-12)
-
-
 # ----------------------------------------------------------------------------- BASELINE configs
 @pytest.mark.parametrize("name", ["laplace", "rmat", "clustered", "uniform"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
@@ -372,6 +360,16 @@ def test_power_iteration_exact_ones_fixed_point():
     cbd.power_iteration_device(h, torch.ones(A.n, dtype=torch.float64, device=DEV), 10,
                                on_step=lambda k, x, s: lams.append(float(s.item()) ** 0.5))
     assert lams == [50.0] * 10
+
+
+@pytest.mark.parametrize("P", [2, 5])
+@pytest.mark.parametrize("name", ["rmat", "clustered", "uniform"])
+def test_column_panels_spmv_fp32(P, name):
+    A = synth.make(name, small=True)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=9)
+    y_ref, R = ref32(A, x)
+    y, h = gpu_spmv(A, x, dtype="f32", col_panels=P)
+    check_rows(y, y_ref, R, 1e-5)
 
 
 @pytest.mark.parametrize("P", [2, 5])
