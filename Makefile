@@ -14,8 +14,9 @@ PKG       := paper_2605_18515_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libcbspmv.so
 
+ABLATION  ?= 0   # 1: profiling build honouring CBSPMV_DEBUG_SKIP
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
-             -Xptxas -v -Iinclude -I$(CSRC) --expt-relaxed-constexpr
+             -Xptxas -v -Iinclude -I$(CSRC) --expt-relaxed-constexpr -DCBSPMV_ABLATION=$(ABLATION)
 CXXFLAGS  := -O3 -std=c++17 -fPIC -Wall -Wextra -Iinclude -I$(CSRC) -I$(CUDA_HOME)/include -pthread
 
 all: synth oracle lib

@@ -114,16 +114,20 @@ __device__ __forceinline__ V ldg_x(const V *p, uint64_t pol) {
   return v;
 }
 
-// Ablation knob for profiling only (env CBSPMV_DEBUG_SKIP, a kernel argument held in a
-// register): bit 0 drops the y atomics, bit 1 replaces the x gathers, bit 2 skips the item
-// processing, bit 3 skips the gather loop.  0 in production.
+// Ablation knob for profiling only: built with -DCBSPMV_ABLATION=1 the env CBSPMV_DEBUG_SKIP
+// (a kernel argument) drops the y atomics (bit 0), replaces the x gathers (bit 1), skips the item
+// processing (bit 2) or the tile copies (bit 3).  In the production build every test folds away.
+#ifndef CBSPMV_ABLATION
+#define CBSPMV_ABLATION 0
+#endif
 struct Dbg {
-  int skip;
+  int skip_;
+  __device__ __forceinline__ int skip() const { return CBSPMV_ABLATION ? skip_ : 0; }
 };
 
 template <typename V>
 __device__ __forceinline__ void red_add(V *p, V v, Dbg dbg) {
-  if (dbg.skip & 1) {
+  if (dbg.skip() & 1) {
     if (v == V(12345.678)) *p = v;  // keep the value live without the atomic
     return;
   }
@@ -174,7 +178,7 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   if (r.valid) {
     if constexpr (AGG) {
       const uint32_t c = reinterpret_cast<const uint32_t *>(page + d.y)[col];
-      r.xv = (dbg.skip & 2) ? V(1) + V(c & 1) : ldg_x(x + c, xpol);
+      r.xv = (dbg.skip() & 2) ? V(1) + V(c & 1) : ldg_x(x + c, xpol);
     } else {
       r.xv = xbuf[(hb + mi) * 16 + col];
     }
@@ -200,7 +204,7 @@ __device__ __forceinline__ const V *warp_tile(const uint8_t *page, const uint4 &
     const int c = lane & 15;
     if (lane < 16 && c < d_ncols(d)) {
       const uint32_t col = reinterpret_cast<const uint32_t *>(page + d.y)[c];
-      scratch[c] = (dbg.skip & 2) ? V(1) + V(col & 1) : __ldg(x + col);
+      scratch[c] = (dbg.skip() & 2) ? V(1) + V(col & 1) : __ldg(x + col);
     }
     __syncwarp();
   }
@@ -299,11 +303,11 @@ __device__ __forceinline__ void issue_tiles(const uint4 *descs, uint32_t iw, V *
   const int hb = iw & 0xFFF;
   const int members = (int)((iw >> 14) & 3) + 1;
   const int mem = lane / kChunks, c = (lane % kChunks) * kPer;
-  if (mem < members && !(dbg.skip & 8)) {
+  if (mem < members && !(dbg.skip() & 8)) {
     const uint4 d = descs[hb + mem];
     const int nc = d_ncols(d);
     V *dst = xbuf + (hb + mem) * 16 + c;
-    if (dbg.skip & 2) {
+    if (dbg.skip() & 2) {
       for (int q = 0; q < kPer; q++) dst[q] = V(1);
     } else if (vec16 && c + kPer <= nc) {
       cp_async_16(dst, x + d.y + c, pol);
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     mbar_wait(&full[s], parity);
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
-    const int nitems = (dbg.skip & 4) ? 0 : (int)hdr[1];
+    const int nitems = (dbg.skip() & 4) ? 0 : (int)hdr[1];
     const uint32_t *items = reinterpret_cast<const uint32_t *>(page + hdr[2]);
     V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + hdr[3]);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
