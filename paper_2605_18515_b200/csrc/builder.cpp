@@ -21,9 +21,27 @@
 
 #include "cb_internal.h"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 namespace cb {
+
+namespace {
+// Phase timing of the host pipeline (env CBSPMV_BUILD_TIMING=1 prints to stderr).
+struct PhaseTimer {
+  bool on = std::getenv("CBSPMV_BUILD_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char *what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cbspmv build] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
 
 int resolve_threads(int t) {
   if (t > 0) return t;
@@ -52,6 +70,35 @@ void parallel_for(int64_t n, int threads, int64_t grain, const std::function<voi
 
 namespace {
 
+// Parallel loop over block rows in chunks of roughly equal nnz (power-law matrices put most
+// non-zeros in a few block rows, which fixed-size chunks would hand to one thread).
+void parallel_blockrows(const Csr &A, int B, int64_t blk_m, int threads,
+                        const std::function<void(int64_t, int64_t, int)> &fn) {
+  if (blk_m <= 0) return;
+  const int T = resolve_threads(threads);
+  const int64_t nnz = A.m > 0 ? A.row_ptr[A.m] : 0;
+  const int64_t chunks = std::min<int64_t>(blk_m, (int64_t)T * 32);
+  std::vector<int64_t> cut(1, 0);
+  for (int64_t k = 1; k < chunks; k++) {
+    // first block row whose starting nnz offset reaches k/chunks of the total (also bounded by rows)
+    const int64_t target = nnz / chunks * k;
+    int64_t lo = cut.back(), hi = blk_m;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (A.row_ptr[std::min<int64_t>(A.m, mid * B)] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    const int64_t by_rows = blk_m * k / chunks;
+    const int64_t c = std::max(cut.back(), std::min(lo, std::max(by_rows, cut.back())));
+    if (c > cut.back()) cut.push_back(c);
+  }
+  cut.push_back(blk_m);
+  const int64_t nch = (int64_t)cut.size() - 1;
+  parallel_for(nch, T, 1, [&](int64_t a, int64_t b, int tid) {
+    for (int64_t k = a; k < b; k++) fn(cut[k], cut[k + 1], tid);
+  });
+}
+
 inline double get_val(const Csr &A, int64_t j) {
   return A.val_size == 8 ? ((const double *)A.val)[j] : (double)((const float *)A.val)[j];
 }
@@ -67,35 +114,143 @@ struct Key {
 struct Scratch {
   std::vector<Key> keys;
   std::vector<uint32_t> cols;
+  std::vector<uint32_t> slot;  // per element (indexed j - row_ptr[r0]): its bucket, ~0u for explicit zeros
+  std::vector<uint32_t> cnt;   // per bucket: element count, then placement cursor
+  struct Run { uint32_t bc, bucket, lr; int64_t j0, j1; };
+  std::vector<Run> runs;       // no-agg: maximal same-block-column runs of each row, row-major
+  std::vector<uint32_t> bcs;   // no-agg: sorted distinct block columns of the block row
 };
 
-// Collect the block row's non-zeros as keys; with aggregation, columns are replaced by their
-// rank in C_i (sorted distinct columns of the block row) and C_i is left in s.cols.
-void block_row_keys(const Csr &A, int B, int64_t br, bool agg, Scratch &s) {
-  s.keys.clear();
-  int64_t r0 = br * B, r1 = std::min<int64_t>(A.m, r0 + B);
-  if (agg) {
-    s.cols.clear();
-    for (int64_t r = r0; r < r1; r++)
-      for (int64_t j = A.row_ptr[r]; j < A.row_ptr[r + 1]; j++)
-        if (get_val(A, j) != 0.0) s.cols.push_back((uint32_t)A.col[j]);
-    std::sort(s.cols.begin(), s.cols.end());
-    s.cols.erase(std::unique(s.cols.begin(), s.cols.end()), s.cols.end());
-  }
+// No aggregation: each row's columns are increasing, so its elements form runs of equal block
+// column.  Sorting the (few) distinct run heads gives the block columns; a counting sort of the
+// elements on their block column's index, filled row-major, gives the (bcol, lr, lc) order.
+// Returns false (and does nothing more) when runs are not much rarer than elements (scattered
+// rows): the caller then uses the merge below.
+static bool block_row_keys_plain(const Csr &A, int B, int64_t r0, int64_t r1, Scratch &s) {
+  s.runs.clear();
+  s.bcs.clear();
   for (int64_t r = r0; r < r1; r++) {
-    uint64_t lr = (uint64_t)(r - r0);
-    const uint32_t *cb = s.cols.data(), *ce = cb + s.cols.size(), *cur = cb;
-    for (int64_t j = A.row_ptr[r]; j < A.row_ptr[r + 1]; j++) {
-      if (get_val(A, j) == 0.0) continue;
-      uint64_t c = (uint64_t)A.col[j];
-      if (agg) {  // columns of a row are increasing: advance the rank cursor monotonically
-        cur = std::lower_bound(cur, ce, (uint32_t)c);
-        c = (uint64_t)(cur - cb);
-      }
-      s.keys.push_back({((c / B) << 8) | (lr << 4) | (c % B), j});
+    int64_t j = A.row_ptr[r], e = A.row_ptr[r + 1];
+    while (j < e) {
+      uint32_t bc = (uint32_t)(A.col[j] / B);
+      int64_t j1 = j + 1;
+      while (j1 < e && (uint32_t)(A.col[j1] / B) == bc) j1++;
+      s.runs.push_back({bc, 0, (uint32_t)(r - r0), j, j1});
+      s.bcs.push_back(bc);
+      j = j1;
     }
   }
-  std::sort(s.keys.begin(), s.keys.end());
+  int64_t total = A.row_ptr[r1] - A.row_ptr[r0];
+  if (s.runs.size() > 64 && (int64_t)s.runs.size() * 4 > total) return false;
+  std::sort(s.bcs.begin(), s.bcs.end());
+  s.bcs.erase(std::unique(s.bcs.begin(), s.bcs.end()), s.bcs.end());
+  s.cnt.assign(s.bcs.size() + 1, 0);
+  const uint32_t *b0 = s.bcs.data(), *be = b0 + s.bcs.size();
+  size_t k = 0;
+  uint32_t lr = ~0u;
+  const uint32_t *cur = b0;
+  for (auto &run : s.runs) {
+    if (run.lr != lr) { cur = b0; lr = run.lr; }  // new row: reset the monotone cursor
+    cur = std::lower_bound(cur, be, run.bc);
+    run.bucket = (uint32_t)(cur - b0);
+    uint32_t nz = 0;
+    for (int64_t j = run.j0; j < run.j1; j++) nz += get_val(A, j) != 0.0;
+    s.cnt[run.bucket + 1] += nz;
+    k += nz;
+  }
+  for (size_t b = 0; b < s.bcs.size(); b++) s.cnt[b + 1] += s.cnt[b];
+  s.keys.resize(k);
+  for (auto &run : s.runs) {
+    uint64_t hi = ((uint64_t)run.bc << 8) | ((uint64_t)run.lr << 4);
+    for (int64_t j = run.j0; j < run.j1; j++)
+      if (get_val(A, j) != 0.0) s.keys[s.cnt[run.bucket]++] = {hi | (uint64_t)(A.col[j] % B), j};
+  }
+  return true;
+}
+
+// Collect the block row's non-zeros as keys sorted by (bcol, lr, lc); with aggregation, columns
+// are replaced by their rank in C_i (sorted distinct columns of the block row) and C_i is
+// left in s.cols.  The rows of a canonical CSR are column-sorted, so a B-way merge of the block
+// row's rows visits its elements in column order: that yields each element's column rank (agg)
+// or the index of its distinct block column (no agg), and a counting sort on that bucket, filled
+// in row-major order, gives the (bcol, lr, lc) order in O(k log B) without a comparison sort.
+void block_row_keys(const Csr &A, int B, int64_t br, bool agg, Scratch &s) {
+  s.keys.clear();
+  s.cols.clear();
+  int64_t r0 = br * B, r1 = std::min<int64_t>(A.m, r0 + B);
+  if (!agg && block_row_keys_plain(A, B, r0, r1, s)) return;
+  int64_t base = A.row_ptr[r0], total = A.row_ptr[r1] - base;
+  if (total == 0) return;
+  s.slot.resize((size_t)total);
+  struct Cur { uint32_t col; int32_t r; int64_t j; };
+  Cur heap[32];
+  int hn = 0;
+  auto less = [](const Cur &a, const Cur &b) { return a.col < b.col || (a.col == b.col && a.r < b.r); };
+  auto push = [&](Cur c) {
+    int i = hn++;
+    while (i > 0) {
+      int p = (i - 1) >> 1;
+      if (!less(c, heap[p])) break;
+      heap[i] = heap[p]; i = p;
+    }
+    heap[i] = c;
+  };
+  auto sift_top = [&]() {  // heap[0] replaced; restore the heap property
+    Cur c = heap[0];
+    int i = 0;
+    for (;;) {
+      int l = 2 * i + 1;
+      if (l >= hn) break;
+      int m = (l + 1 < hn && less(heap[l + 1], heap[l])) ? l + 1 : l;
+      if (!less(heap[m], c)) break;
+      heap[i] = heap[m]; i = m;
+    }
+    heap[i] = c;
+  };
+  for (int64_t r = r0; r < r1; r++)
+    if (A.row_ptr[r] < A.row_ptr[r + 1]) push({(uint32_t)A.col[A.row_ptr[r]], (int32_t)(r - r0), A.row_ptr[r]});
+  uint32_t nbuck = 0, ndist = 0;
+  uint64_t last_col = ~0ull, last_bc = ~0ull;
+  while (hn > 0) {
+    Cur c = heap[0];
+    int64_t j = c.j;
+    if (get_val(A, j) != 0.0) {
+      if (agg) {
+        if (c.col != last_col) { s.cols.push_back(c.col); last_col = c.col; ndist++; }
+        s.slot[j - base] = ndist - 1;  // rank in C_i
+      } else {
+        uint64_t bc = c.col / (uint32_t)B;
+        if (bc != last_bc) { last_bc = bc; nbuck++; }
+        s.slot[j - base] = nbuck - 1;
+      }
+    } else {
+      s.slot[j - base] = ~0u;
+    }
+    int64_t end = A.row_ptr[r0 + c.r + 1];
+    if (j + 1 < end) {
+      heap[0] = {(uint32_t)A.col[j + 1], c.r, j + 1};
+    } else {
+      heap[0] = heap[--hn];
+    }
+    if (hn > 0) sift_top();
+  }
+  if (agg) nbuck = (ndist + B - 1) / B;
+  s.cnt.assign((size_t)nbuck + 1, 0);
+  uint32_t div = agg ? (uint32_t)B : 1u;
+  size_t k = 0;
+  for (int64_t t = 0; t < total; t++)
+    if (s.slot[t] != ~0u) { s.cnt[s.slot[t] / div + 1]++; k++; }
+  for (uint32_t b = 0; b < nbuck; b++) s.cnt[b + 1] += s.cnt[b];
+  s.keys.resize(k);
+  for (int64_t r = r0; r < r1; r++) {
+    uint64_t lr = (uint64_t)(r - r0);
+    for (int64_t j = A.row_ptr[r]; j < A.row_ptr[r + 1]; j++) {
+      uint32_t sl = s.slot[j - base];
+      if (sl == ~0u) continue;
+      uint64_t c = agg ? (uint64_t)sl : (uint64_t)A.col[j];
+      s.keys[s.cnt[sl / div]++] = {((c / B) << 8) | (lr << 4) | (c % B), j};
+    }
+  }
 }
 
 inline int64_t padding(int64_t idx_bytes, int64_t S) {  // Alg. 3 lines 6-7
@@ -121,8 +276,10 @@ inline void put_val(uint8_t *dst, int64_t i, double v, int64_t S) {
   else { float f = (float)v; std::memcpy(dst + 4 * i, &f, 4); }
 }
 
-// Pack one block's record at dst (zero-filled); e = its keys (sorted), k = nnz.
+// Pack one block's record at dst (cleared here first, so padding is zero); e = its keys (sorted),
+// k = nnz.
 void pack_record(const Csr &A, int B, int64_t S, int type, const Key *e, int64_t k, uint8_t *dst) {
+  std::memset(dst, 0, (size_t)record_bytes(type, k, B, S));
   if (type == CBSPMV_FMT_COO) {
     for (int64_t t = 0; t < k; t++) {
       uint32_t lr = (e[t].key >> 4) & 15, lc = e[t].key & 15;
@@ -210,7 +367,7 @@ int canonical_check(const Csr &A, int threads, int64_t *nnz, std::string *err) {
 void pre_stats(const Csr &A, const cbspmv_options_t &o, int64_t blk_m, std::vector<Scratch> &scr,
                int64_t *nb_pre, int64_t *ss_count) {
   std::vector<int64_t> pre_nb(blk_m), pre_ss(blk_m);
-  parallel_for(blk_m, (int)scr.size(), 64, [&](int64_t lo, int64_t hi, int tid) {
+  parallel_blockrows(A, o.blk, blk_m, (int)scr.size(), [&](int64_t lo, int64_t hi, int tid) {
     Scratch &s = scr[tid];
     for (int64_t br = lo; br < hi; br++) {
       block_row_keys(A, o.blk, br, false, s);
@@ -261,17 +418,20 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
   c = Canon();
   c.m = A.m; c.n = A.n; c.blk = B; c.val_size = (int)S; c.W = W;
   c.blk_m = (A.m + B - 1) / B;
+  PhaseTimer tm;
   st = canonical_check(A, threads, &c.nnz, err);   // a1
+  tm.lap("a1 canonical check");
   if (st != CBSPMV_OK) return st;
   const int T = resolve_threads(threads);
   std::vector<Scratch> scr(T);
   pre_stats(A, o, c.blk_m, scr, &c.nb_pre, &c.ss_count);   // a3
+  tm.lap("a3 block statistics");
   c.agg = o.agg_mode >= 0 ? o.agg_mode : decide_agg(c.nb_pre, c.ss_count, o);
   const bool agg = c.agg != 0;
 
   // a4 + a5 sizing pass: blocks, restore entries and record bytes per block row.
   std::vector<int64_t> br_nb(c.blk_m + 1, 0), br_res(c.blk_m + 1, 0), br_bytes(c.blk_m + 1, 0);
-  parallel_for(c.blk_m, T, 64, [&](int64_t lo, int64_t hi, int tid) {
+  parallel_blockrows(A, B, c.blk_m, T, [&](int64_t lo, int64_t hi, int tid) {
     Scratch &s = scr[tid];
     for (int64_t br = lo; br < hi; br++) {
       block_row_keys(A, B, br, agg, s);
@@ -290,18 +450,19 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
   }
   const int64_t nb = br_nb[c.blk_m];
   c.nb = nb;
-  c.mtx.assign((size_t)br_bytes[c.blk_m], 0);
+  c.mtx.resize((size_t)br_bytes[c.blk_m]);  // not zeroed: pack_record clears each record
   if (agg) {
     c.restore.resize((size_t)br_res[c.blk_m]);
     c.cols_offset.resize((size_t)c.blk_m + 1);
     for (int64_t br = 0; br <= c.blk_m; br++) c.cols_offset[br] = (uint64_t)br_res[br];
   }
 
+  tm.lap("a4+a5 sizing pass");
   // a6 fill pass: natural-order metadata, restore_cols, packed records at VP = byte offset.
   std::vector<int32_t> nbr(nb), nbc(nb), nnzb(nb);
   std::vector<uint8_t> ntype(nb);
   std::vector<uint64_t> nvp(nb);
-  parallel_for(c.blk_m, T, 64, [&](int64_t lo, int64_t hi, int tid) {
+  parallel_blockrows(A, B, c.blk_m, T, [&](int64_t lo, int64_t hi, int tid) {
     Scratch &s = scr[tid];
     for (int64_t br = lo; br < hi; br++) {
       block_row_keys(A, B, br, agg, s);
@@ -322,6 +483,7 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
   });
   for (int64_t b = 0; b < nb; b++) c.fmt_count[ntype[b]]++;
 
+  tm.lap("a6 fill pass");
   // a7. TB-Load-Balance (Alg. 2).
   const int64_t TB = (nb + W - 1) / W;
   c.T = TB;
@@ -377,6 +539,7 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
       c.tb_load[t] = c.tb_load_nat[t];
     }
   }
+  tm.lap("a7 Alg. 2 greedy");
   // permute the five high-level arrays (vp_per_blk[i] <- vp_per_blk_old[ori])
   c.br.resize(nb); c.bc.resize(nb); c.nnzb.resize(nb); c.type.resize(nb); c.vp.resize(nb);
   parallel_for(nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
@@ -385,6 +548,7 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
       c.br[i] = nbr[b]; c.bc[i] = nbc[b]; c.nnzb[i] = nnzb[b]; c.type[i] = ntype[b]; c.vp[i] = nvp[b];
     }
   });
+  tm.lap("a7 permute");
   return CBSPMV_OK;
 }
 
@@ -423,6 +587,7 @@ void free_stream(Stream *s) {
 
 int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::string *err) {
   const int T = resolve_threads(threads);
+  PhaseTimer tm;
   std::vector<int64_t> rec(c.nb);
   std::vector<int32_t> ncol(c.nb);
   parallel_for(c.nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
@@ -477,6 +642,7 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
   page_tb.push_back(c.T);
   const int64_t npages = (int64_t)off.size() - 1;
 
+  tm.lap("stream: page plan");
   s->nbytes = total;
   s->page_off = off;
   if (total > 0) {
@@ -569,6 +735,7 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
       }
     }
   });
+  tm.lap("stream: fill pages");
   return CBSPMV_OK;
 }
 

@@ -3,6 +3,8 @@
 #pragma once
 #include <cstdint>
 #include <functional>
+#include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -55,6 +57,18 @@ inline uint32_t pack_w(uint32_t nnz, uint32_t type, uint32_t ncols, bool head, u
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
+// Allocator whose value-initialisation is a no-op: resize() of a multi-GB byte buffer leaves the
+// pages untouched, so their first touch happens in the parallel fill threads.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U> struct rebind { using other = NoInitAlloc<U>; };
+  NoInitAlloc() = default;
+  template <class U> NoInitAlloc(const NoInitAlloc<U> &) noexcept {}
+  template <class U> void construct(U *p) noexcept { ::new ((void *)p) U; }
+  template <class U, class... Args> void construct(U *p, Args &&...a) { ::new ((void *)p) U(std::forward<Args>(a)...); }
+};
+using ByteBuf = std::vector<uint8_t, NoInitAlloc<uint8_t>>;
+
 // ---------------------------------------------------------------------------
 // Canonical format (slot order), byte-identical to the paper-literal CPU reference build
 // (checked by tests/test_builder_parity.py).
@@ -65,7 +79,7 @@ struct Canon {
   std::vector<int32_t> br, bc, nnzb;
   std::vector<uint8_t> type;
   std::vector<uint64_t> vp;
-  std::vector<uint8_t> mtx;
+  ByteBuf mtx;  // every byte written by pack_record (records and their padding)
   std::vector<uint32_t> restore;
   std::vector<uint64_t> cols_offset;
   std::vector<int64_t> tb_ptr, tb_load, tb_load_nat;
