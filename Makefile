@@ -31,16 +31,15 @@ synth/libsynth.so: synth/synth.c
 oracle/liboracle.so: oracle/oracle.c
 	$(CC) -O2 -fPIC -shared -Wall -Wextra -std=c11 -o $@ $<
 
-$(CSRC)/builder.o: $(CSRC)/builder.cpp $(CSRC)/cb_internal.h include/cbspmv.h
-	$(CXX) $(CXXFLAGS) -c -o $@ $<
+HOST_OBJS := $(CSRC)/builder.o $(CSRC)/capi.o $(CSRC)/mmio.o $(CSRC)/container.o
 
-$(CSRC)/capi.o: $(CSRC)/capi.cpp $(CSRC)/cb_internal.h include/cbspmv.h
+$(CSRC)/%.o: $(CSRC)/%.cpp $(CSRC)/cb_internal.h include/cbspmv.h
 	$(CXX) $(CXXFLAGS) -c -o $@ $<
 
 $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/cb_internal.h include/cbspmv.h
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
 
-$(LIB): $(CSRC)/builder.o $(CSRC)/capi.o $(CSRC)/kernels.o
+$(LIB): $(HOST_OBJS) $(CSRC)/kernels.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lpthread
 
 clean:

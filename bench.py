@@ -2,7 +2,7 @@
 """CB-SpMV benchmark (BASELINE.json metric) — one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat|clustered|laplace|uniform]
-                    [--dtype f64|f32] [--impl cb|reference]
+                    [--dtype f64|f32|f32f64] [--impl cb|reference]
 
 Default workload: BASELINE configs[3] (block-clustered, 2^22 rows, ~407M nnz,
 fp64) — the large synthetic matrix whose HBM roofline the metric asks for and
@@ -202,7 +202,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
     A, (r0, r1), nnz_total = make_matrix(args.config, rank, world)
     gen_s = time.perf_counter() - t0
     agg = dist.global_agg(A, lambda a: allreduce(a), dtype=args.dtype) if world > 1 else -1
-    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
     h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0)
     info = h.info
     x_host = synth.vector(A.n, synth.VEC_UNIFORM, seed=7)
@@ -254,7 +254,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
     cold_ms = statistics.median(cold) if cold else None
 
     # ---- end to end through the public API with host buffers (pinned)
-    vt = np.float64 if args.dtype == "f64" else np.float32
+    vt = np.float32 if args.dtype == "f32" else np.float64
     xh = torch.from_numpy(x_host.astype(vt)).pin_memory().numpy()
     yh = torch.empty(A.m, dtype=tdt).pin_memory().numpy()
     cb.spmv_host(h, xh, yh)
@@ -276,7 +276,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
         cpu = cpu_baseline(A, x_host, args.dtype)
     also = {}
     if world == 1 and args.also:
-        names = [n for n in args.also.split(",") if n and n != args.config and n != "uniform"]
+        names = [n for n in args.also.split(",") if n and n not in (args.config, "uniform", "none")]
         cb.destroy(h)
         also = measure_also(names, args.dtype, args.steps, max(args.warmup, 3), local_rank)
 
@@ -324,7 +324,7 @@ def measure_also(names, dtype, steps, warmup, local_rank):
     import synth
     out = {}
     dev = torch.device("cuda", local_rank)
-    tdt = torch.float64 if dtype == "f64" else torch.float32
+    tdt = torch.float32 if dtype == "f32" else torch.float64
     for name in names:
         A = synth.make(name)
         h = cb.build(A, dtype=dtype, device=local_rank, keep_host=0)
@@ -379,7 +379,7 @@ def run_power(args, rank, world, local_rank):
     agg = dist.global_agg(A, lambda a: _allreduce_np(a, dev, world), dtype=args.dtype) if world > 1 else -1
     h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0)
     info = h.info
-    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
     x0 = torch.ones(A.n, dtype=tdt, device=dev)
     dist.power_iteration_device(h, x0, max(args.warmup, 3), world)
     torch.cuda.synchronize()
@@ -442,8 +442,9 @@ def cpu_baseline(A, x, dtype):
     import oracle
     import synth
     from paper_2605_18515_b200.dist import slice_rows
-    if dtype == "f32":
+    if dtype in ("f32", "f32f64"):  # the oracle in fp64 on the rounded inputs
         A = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
+    if dtype == "f32":
         x = x.astype(np.float32).astype(np.float64)
     t0 = time.perf_counter()
     oracle.spmv_csr(A, x)
@@ -474,7 +475,7 @@ def main():
     ap.add_argument("--config", default="clustered", choices=list(WORKLOAD))
     ap.add_argument("--also", default="rmat,laplace",
                     help="other BASELINE workloads timed the same way on N=1 (comma list, '' for none)")
-    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32", "f32f64"])
     ap.add_argument("--impl", default="cb", choices=["cb", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -41,10 +41,16 @@ typedef enum {
   CBSPMV_ENOMEM = 3,      /* host or device allocation failed */
   CBSPMV_ECUDA = 4,       /* a CUDA runtime call failed (detail in cbspmv_last_error) */
   CBSPMV_EDIM = 5,        /* pointer alignment / device mismatch */
-  CBSPMV_EUNSUPPORTED = 6 /* e.g. device call on a host-only handle, blk != 16 on device */
+  CBSPMV_EUNSUPPORTED = 6, /* e.g. device call on a host-only handle, blk != 16 on device */
+  CBSPMV_EIO = 7,          /* a file could not be opened, read or written */
+  CBSPMV_EFORMAT = 8       /* malformed Matrix Market or CBSM file content */
 } cbspmv_status_t;
 
-typedef enum { CBSPMV_F64 = 0, CBSPMV_F32 = 1 } cbspmv_dtype_t;
+/* Value types.  CBSPMV_F32F64 is the mixed variant the paper names without defining (P:251,
+ * P:379; reading R-24): matrix values stored as fp32 in the records (size(Val) = 4, the fp32
+ * layout), x, y and every product / accumulation in fp64.  Its result equals the fp64 product
+ * of the fp32-rounded matrix with x within the fp64 tolerance. */
+typedef enum { CBSPMV_F64 = 0, CBSPMV_F32 = 1, CBSPMV_F32F64 = 2 } cbspmv_dtype_t;
 
 /* Sub-block storage formats. */
 enum { CBSPMV_FMT_COO = 0, CBSPMV_FMT_CSR = 1, CBSPMV_FMT_DENSE = 2 };
@@ -90,7 +96,7 @@ typedef struct {
   int64_t n_restore;              /* |restore_cols| (u32 each) */
   int64_t meta_bytes;             /* 21 B per block: br, bc, nnz (i32), type (u8), vp (u64) */
   int64_t alg_bytes;              /* algorithmic bytes of one SpMV: meta + mtx + 4*restore +
-                                     8*(blk_m+1 if agg) + size(Val)*(n + m) */
+                                     8*(blk_m+1 if agg) + size(x elem)*(n + m) */
   int64_t dev_stream_bytes;       /* bytes of the device page stream */
   int64_t n_pages;                /* device pages */
   int64_t dev_bytes;              /* all device memory owned by the handle */
@@ -129,7 +135,8 @@ cbspmv_status_t cbspmv_default_options(cbspmv_options_t *opts);
  * uploads it in one copy ("transferred to the GPU in a single operation").
  *   row_ptr: m+1 int64, non-decreasing, row_ptr[0] = 0
  *   col_idx: nnz int32 in [0, n), strictly increasing within each row
- *   vals:    nnz values of dtype (double or float); explicit zeros are dropped
+ *   vals:    nnz values: double (CBSPMV_F64) or float (CBSPMV_F32, CBSPMV_F32F64); explicit
+ *            zeros are dropped
  *   opts:    NULL = defaults
  *   stream:  stream for the upload; build returns after the upload completed
  * The CSR is read during the call only.  On error *out is NULL. */
@@ -139,8 +146,8 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
 
 /* y := A·x (Alg. 3 / Alg. 4 semantics).  Zeroes y, then one
  * persistent kernel streams the page stream and adds every block's products
- * into y (R-16).  x_dev: n values, y_dev: m values of the handle's dtype,
- * 8-byte (f64) / 4-byte (f32) aligned, not aliasing. */
+ * into y (R-16).  x_dev: n values, y_dev: m values, double (CBSPMV_F64,
+ * CBSPMV_F32F64) or float (CBSPMV_F32), aligned to their size, not aliasing. */
 cbspmv_status_t cbspmv_spmv(cbspmv_handle_t h, const void *x_dev, void *y_dev, void *stream);
 
 /* y += A·x (the kernel alone, no zeroing). */
@@ -157,8 +164,8 @@ cbspmv_status_t cbspmv_spmv_scaled(cbspmv_handle_t h, const void *x_dev, const d
  * and synchronises the stream before returning. */
 cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_host, void *stream);
 
-/* *out_dev (one double on the device) := sum_i v_i^2 over len values of dtype
- * (the power-iteration finalize step). */
+/* *out_dev (one double on the device) := sum_i v_i^2 over len vector values of dtype
+ * (float for CBSPMV_F32, else double; the power-iteration finalize step). */
 cbspmv_status_t cbspmv_sumsq(const void *v_dev, int64_t len, cbspmv_dtype_t dtype, double *out_dev,
                              int32_t device, void *stream);
 
@@ -186,6 +193,53 @@ cbspmv_status_t cbspmv_export_panel(cbspmv_handle_t h, int32_t k, cbspmv_export_
  * verification; synchronous; single-panel handles only). */
 cbspmv_status_t cbspmv_download_stream(cbspmv_handle_t h, void *stream_host, size_t stream_bytes,
                                        uint64_t *page_off_host, size_t n_page_off);
+
+/* ------------------------------------------------------------------ files
+ * Host CSR returned by cbspmv_mm_read; its arrays are owned by the library and released
+ * with cbspmv_csr_free. */
+typedef struct {
+  int64_t m, n, nnz;
+  int64_t *row_ptr;   /* m + 1 */
+  int32_t *col_idx;   /* nnz, strictly increasing within each row */
+  double *vals;       /* nnz, finite and non-zero */
+} cbspmv_csr_t;
+
+/* Read a Matrix Market coordinate file (the inputs of the paper's evaluation are SuiteSparse
+ * Matrix Market files; semantics of SPEC.md S:26-81): banner
+ * "%%MatrixMarket matrix coordinate <real|double|integer|pattern> <general|symmetric|
+ * skew-symmetric|hermitian>", 1-based indices.  Off-diagonal entries of symmetric / hermitian
+ * files are mirrored (negated for skew-symmetric), pattern entries are 1.0, duplicates are
+ * summed in file order (each entry, then its mirror), entries that are exactly zero after
+ * summation are dropped, rows are column-sorted: the result is a canonical CSR accepted by
+ * cbspmv_build.  Errors: EIO (open/read), EFORMAT (banner, size line, entry count mismatch,
+ * malformed entry, index outside the declared size), EINVAL (non-finite value), EUNSUPPORTED
+ * (complex field, array format, n > INT32_MAX).  On error *out is zeroed. */
+cbspmv_status_t cbspmv_mm_read(const char *path, cbspmv_csr_t *out);
+
+/* Write a CSR as "%%MatrixMarket matrix coordinate real general" with the shortest decimal form
+ * that round-trips each double, so cbspmv_mm_read(cbspmv_mm_write(A)) == A bit for bit for a
+ * canonical A.  Errors: EINVAL (arguments), EIO. */
+cbspmv_status_t cbspmv_mm_write(const char *path, int64_t m, int64_t n, const int64_t *row_ptr,
+                                const int32_t *col_idx, const double *vals);
+
+/* Release the arrays of a CSR returned by cbspmv_mm_read (NULL-safe, idempotent). */
+cbspmv_status_t cbspmv_csr_free(cbspmv_csr_t *csr);
+
+/* Save the canonical format of every column panel in the CBSM container (magic
+ * "CBSM", version 1, the five per-block arrays, cols_offset / restore_cols, mtx_data; all
+ * little-endian) followed by an extension block holding dtype, warps_per_tb, the panel's
+ * columns, nnz / nb_pre / ss_count and the Alg. 2 schedule (tb_ptr and per-TB loads) — layout
+ * in container.cpp.  Requires keep_host = 1.  Errors: EUNSUPPORTED, EIO. */
+cbspmv_status_t cbspmv_save(cbspmv_handle_t h, const char *path);
+
+/* Load a CBSM file written by cbspmv_save (or a plain version-1 container: one fp64 panel,
+ * thread blocks = consecutive groups of 8 blocks) and, for opts->device >= 0, lay it out as
+ * the device page stream and upload it — steps a1..a7 are not re-run (the
+ * preprocessing is a one-off cost).  Every record is decoded and its indices checked against
+ * the matrix bounds before upload.  From opts only device, host_threads and keep_host are used.
+ * Errors: EIO, EFORMAT (bad magic, truncated or inconsistent content), ENOMEM, ECUDA. */
+cbspmv_status_t cbspmv_load(const char *path, const cbspmv_options_t *opts, void *stream,
+                            cbspmv_handle_t *out);
 
 /* Free everything the handle owns.  NULL-safe. */
 cbspmv_status_t cbspmv_destroy(cbspmv_handle_t h);

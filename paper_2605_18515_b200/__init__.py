@@ -14,6 +14,8 @@ Names mirror the C ABI without the ``cbspmv_`` prefix::
     spmv_host(h, x_np, y_np)                 # cbspmv_spmv_host    host buffers, end to end
     sumsq(v, out)                            # cbspmv_sumsq
     get_info(h), export(h), download_stream(h), destroy(h)
+    A = mm_read(path); mm_write(path, A)     # Matrix Market files
+    save(h, path); h = load(path, device=0)  # CBSM container
 
 Device vectors are torch CUDA tensors (or raw integer device pointers); the
 stream defaults to torch's current stream on the handle's device.
@@ -29,9 +31,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcbspmv.so")
 _lib = None
 
-F64, F32 = 0, 1
+F64, F32, F32F64 = 0, 1, 2  # F32F64: fp32 matrix values, fp64 x / y / accumulation (R-24)
+DTYPES = {"f64": F64, "f32": F32, "f32f64": F32F64, F64: F64, F32: F32, F32F64: F32F64}
 FMT_COO, FMT_CSR, FMT_DENSE = 0, 1, 2
-STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSORTED", 3: "ENOMEM", 4: "ECUDA", 5: "EDIM", 6: "EUNSUPPORTED"}
+STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSORTED", 3: "ENOMEM", 4: "ECUDA", 5: "EDIM", 6: "EUNSUPPORTED", 7: "EIO",
+          8: "EFORMAT"}
 
 
 class Options(ctypes.Structure):
@@ -67,6 +71,21 @@ class Export(ctypes.Structure):
     ]
 
 
+class CsrC(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("n", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row_ptr", ctypes.POINTER(ctypes.c_int64)), ("col_idx", ctypes.POINTER(ctypes.c_int32)),
+                ("vals", ctypes.POINTER(ctypes.c_double))]
+
+
+class HostCSR:
+    """A host CSR (``m, n, nnz, row_ptr, col, val``) as returned by ``mm_read``; ``build`` accepts it."""
+
+    def __init__(self, m, n, row_ptr, col, val):
+        self.m, self.n = int(m), int(n)
+        self.row_ptr, self.col, self.val = row_ptr, col, val
+        self.nnz = int(row_ptr[-1]) if len(row_ptr) else 0
+
+
 def lib():
     """Load libcbspmv.so (raises if it was not built: there is no fallback path)."""
     global _lib
@@ -93,6 +112,11 @@ def lib():
             "cbspmv_export_panel": ([H, i32, ctypes.POINTER(Export)], i32),
             "cbspmv_download_stream": ([H, vp, ctypes.c_size_t, vp, ctypes.c_size_t], i32),
             "cbspmv_destroy": ([H], i32),
+            "cbspmv_mm_read": ([ctypes.c_char_p, ctypes.POINTER(CsrC)], i32),
+            "cbspmv_mm_write": ([ctypes.c_char_p, i64, i64, vp, vp, vp], i32),
+            "cbspmv_csr_free": ([ctypes.POINTER(CsrC)], i32),
+            "cbspmv_save": ([H, ctypes.c_char_p], i32),
+            "cbspmv_load": ([ctypes.c_char_p, ctypes.POINTER(Options), vp, ctypes.POINTER(H)], i32),
             "cbspmv_status_string": ([i32], ctypes.c_char_p),
             "cbspmv_last_error": ([], ctypes.c_char_p),
             "cbspmv_version": ([], i32),
@@ -171,13 +195,23 @@ class Handle:
             pass
 
 
+def value_dtype(dt: int):
+    """numpy type of the stored matrix values."""
+    return np.float64 if dt == F64 else np.float32
+
+
+def vector_dtype(dt: int):
+    """numpy type of x and y."""
+    return np.float32 if dt == F32 else np.float64
+
+
 def build(A, dtype: str | int = "f64", device: int = 0, stream=None, **opts) -> Handle:
     """cbspmv_build on a host CSR (``A.m, A.n, A.row_ptr, A.col, A.val``)."""
-    dt = {"f64": F64, "f32": F32, F64: F64, F32: F32}[dtype]
+    dt = DTYPES[dtype]
     o = default_options(device=device, **opts)
     rp = np.ascontiguousarray(A.row_ptr, np.int64)
     col = np.ascontiguousarray(A.col, np.int32)
-    val = np.ascontiguousarray(A.val, np.float64 if dt == F64 else np.float32)
+    val = np.ascontiguousarray(A.val, value_dtype(dt))
     h = ctypes.c_void_p()
     st = None
     if device >= 0:
@@ -189,11 +223,11 @@ def build(A, dtype: str | int = "f64", device: int = 0, stream=None, **opts) -> 
 
 def block_stats(A, dtype: str | int = "f64", **opts) -> tuple[int, int]:
     """cbspmv_block_stats: (non-empty blocks, super-sparse blocks) before aggregation."""
-    dt = {"f64": F64, "f32": F32, F64: F64, F32: F32}[dtype]
+    dt = DTYPES[dtype]
     o = default_options(**opts)
     rp = np.ascontiguousarray(A.row_ptr, np.int64)
     col = np.ascontiguousarray(A.col, np.int32)
-    val = np.ascontiguousarray(A.val, np.float64 if dt == F64 else np.float32)
+    val = np.ascontiguousarray(A.val, value_dtype(dt))
     nb, ss = ctypes.c_int64(), ctypes.c_int64()
     _check(lib().cbspmv_block_stats(A.m, A.n, int(rp[-1]) if len(rp) else 0, rp.ctypes.data, col.ctypes.data,
                                     val.ctypes.data, dt, ctypes.byref(o), ctypes.byref(nb), ctypes.byref(ss)),
@@ -223,7 +257,7 @@ def spmv_scaled(h: Handle, x, sumsq_dev, y, stream=None) -> None:
 
 
 def spmv_host(h: Handle, x: np.ndarray, y: np.ndarray, stream=None) -> None:
-    vt = np.float64 if h.dtype == F64 else np.float32
+    vt = vector_dtype(h.dtype)
     if x.dtype != vt or y.dtype != vt or not x.flags.c_contiguous or not y.flags.c_contiguous:
         raise ValueError("host x / y must be contiguous arrays of the handle's dtype")
     if x.size != h.info["n"] or y.size != h.info["m"]:
@@ -281,6 +315,44 @@ def destroy(h: Handle) -> None:
     if h._raw is not None:
         lib().cbspmv_destroy(h._raw)
         h._raw = None
+
+
+def mm_read(path) -> HostCSR:
+    """cbspmv_mm_read: a Matrix Market coordinate file as a canonical host CSR (copied out)."""
+    c = CsrC()
+    _check(lib().cbspmv_mm_read(os.fsencode(path), ctypes.byref(c)), "cbspmv_mm_read")
+    try:
+        rp = np.ctypeslib.as_array(c.row_ptr, shape=(c.m + 1,)).copy()
+        col = np.ctypeslib.as_array(c.col_idx, shape=(max(c.nnz, 1),))[:c.nnz].copy()
+        val = np.ctypeslib.as_array(c.vals, shape=(max(c.nnz, 1),))[:c.nnz].copy()
+        return HostCSR(c.m, c.n, rp, col, val)
+    finally:
+        lib().cbspmv_csr_free(ctypes.byref(c))
+
+
+def mm_write(path, A) -> None:
+    """cbspmv_mm_write: ``A`` (m, n, row_ptr, col, val) as a real general coordinate file."""
+    rp = np.ascontiguousarray(A.row_ptr, np.int64)
+    col = np.ascontiguousarray(A.col, np.int32)
+    val = np.ascontiguousarray(A.val, np.float64)
+    _check(lib().cbspmv_mm_write(os.fsencode(path), A.m, A.n, rp.ctypes.data, col.ctypes.data, val.ctypes.data),
+           "cbspmv_mm_write")
+
+
+def save(h: Handle, path) -> None:
+    """cbspmv_save: the canonical format in the CBSM container (needs keep_host=1)."""
+    _check(lib().cbspmv_save(h.raw, os.fsencode(path)), "cbspmv_save")
+
+
+def load(path, device: int = 0, stream=None, **opts) -> Handle:
+    """cbspmv_load: a CBSM file -> handle (device page stream rebuilt and uploaded; a1..a7 skipped)."""
+    o = default_options(device=device, **opts)
+    h = ctypes.c_void_p()
+    st = _stream(stream, device) if device >= 0 else None
+    _check(lib().cbspmv_load(os.fsencode(path), ctypes.byref(o), st, ctypes.byref(h)), "cbspmv_load")
+    info = Info()
+    _check(lib().cbspmv_get_info(h, ctypes.byref(info)), "cbspmv_get_info")
+    return Handle(h, info.dtype, device)
 
 
 def version() -> int:

@@ -585,7 +585,7 @@ void free_stream(Stream *s) {
   s->bytes = nullptr; s->nbytes = 0; s->page_off.clear();
 }
 
-int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::string *err) {
+int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, std::string *err) {
   const int T = resolve_threads(threads);
   PhaseTimer tm;
   std::vector<int64_t> rec(c.nb);
@@ -613,7 +613,7 @@ int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::stri
   };
   // x tile bytes per block gathered into the stage (non-aggregated matrices only; with aggregation
   // the consumer lanes gather x per element)
-  const int64_t tile = c.agg ? 0 : 16 * (int64_t)c.val_size;
+  const int64_t tile = c.agg ? 0 : 16 * (int64_t)x_size;
   auto stage_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
     return round_up(page_bytes(b0, b1, rec_bytes), 16) + tile * (b1 - b0);
   };

@@ -60,6 +60,11 @@ struct Part {
 };
 
 // Rows x columns [c0, c1) of a canonical CSR (columns keep their global index).
+// dtype -> bytes of one stored matrix value / one x or y element
+inline int val_bytes(int dtype) { return dtype == CBSPMV_F64 ? 8 : 4; }
+inline int vec_bytes(int dtype) { return dtype == CBSPMV_F32 ? 4 : 8; }
+inline bool valid_dtype(int dtype) { return dtype == CBSPMV_F64 || dtype == CBSPMV_F32 || dtype == CBSPMV_F32F64; }
+
 struct SubCsr {
   std::vector<int64_t> rp;
   std::vector<int32_t> col;
@@ -71,7 +76,8 @@ struct SubCsr {
 struct cbspmv_s {
   int device = -1;
   int dtype = CBSPMV_F64;
-  int val_size = 8;
+  int val_size = 8;  // stored matrix values
+  int vec_size = 8;  // x / y elements
   bool has_host = false;
   std::vector<Part> parts;
   cbspmv_info_t info{};
@@ -116,21 +122,19 @@ static void free_device(cbspmv_s *h) {
   h->d_x_tmp = nullptr; h->d_y_tmp = nullptr;
 }
 
-// Build + upload one panel's format (the Fig. 7 pipeline on A[:, c0:c1)).
-static int build_part(const cb::Csr &A, const cbspmv_options_t &o, cudaStream_t cs, Part *P, double *t_up,
-                      std::string *err) {
-  int st = cb::build_canonical(A, o, &P->canon, err);
-  if (st != CBSPMV_OK || o.device < 0) return st;
+// Device page stream of one panel's canonical format, uploaded in one copy (a8).
+static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Part *P, double *t_up,
+                       std::string *err) {
   const cb::Canon &c = P->canon;
   cb::Stream S;
   const char *env = std::getenv("CBSPMV_PAGE_BYTES");
   int cap = env ? std::atoi(env) : cb::kDefaultStageCap;
   cap = (int)cb::round_up(std::max(cap, 1024), 16);
-  st = cb::build_stream(c, cap, o.host_threads, &S, err);
+  int st = cb::build_stream(c, cap, vec_bytes(dtype), o.host_threads, &S, err);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   const int64_t npages = (int64_t)S.page_off.size() - 1;
   CbDevice &D = P->dev;
-  D.device = o.device; D.dtype = A.val_size == 8 ? CBSPMV_F64 : CBSPMV_F32; D.agg = c.agg; D.m = c.m; D.n = c.n;
+  D.device = o.device; D.dtype = dtype; D.agg = c.agg; D.m = c.m; D.n = c.n;
   D.n_pages = npages; D.page_cap = cap;
   st = cb_configure(&D, err);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
@@ -174,9 +178,64 @@ static int build_part(const cb::Csr &A, const cbspmv_options_t &o, cudaStream_t 
   return CBSPMV_OK;
 }
 
-cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
-                             const void *vals, cbspmv_dtype_t dtype, const cbspmv_options_t *opts, void *stream,
-                             cbspmv_handle_t *out) {
+// Build + upload one panel's format (the Fig. 7 pipeline on A[:, c0:c1)).
+static int build_part(const cb::Csr &A, const cbspmv_options_t &o, int dtype, cudaStream_t cs, Part *P,
+                      double *t_up, std::string *err) {
+  int st = cb::build_canonical(A, o, &P->canon, err);
+  if (st != CBSPMV_OK || o.device < 0) return st;
+  return upload_part(o, dtype, cs, P, t_up, err);
+}
+
+// info: sums over panels; drops the host arrays unless keep_host
+static void fill_info(cbspmv_s *h, int64_t m, int64_t n, double t0, double t_up, bool keep_host) {
+  const int P = (int)h->parts.size();
+  const int dtype = h->dtype;
+  cbspmv_info_t &I = h->info;
+  I.m = m; I.n = n; I.dtype = dtype; I.n_panels = P;
+  std::vector<int64_t> loads, loads_nat;
+  for (const Part &p : h->parts) {
+    const cb::Canon &c = p.canon;
+    I.nnz += c.nnz; I.nb += c.nb; I.nb_pre += c.nb_pre; I.ss_count += c.ss_count; I.agg |= c.agg;
+    I.blk_m = c.blk_m;
+    for (int k = 0; k < 3; k++) I.fmt_count[k] += c.fmt_count[k];
+    I.T += c.T;
+    I.mtx_bytes += (int64_t)c.mtx.size();
+    I.n_restore += (int64_t)c.restore.size();
+    I.meta_bytes += 21 * c.nb;
+    I.alg_bytes += 21 * c.nb + (int64_t)c.mtx.size() + 4 * (int64_t)c.restore.size() + (c.agg ? 8 * (c.blk_m + 1) : 0);
+    loads.insert(loads.end(), c.tb_load.begin(), c.tb_load.end());
+    loads_nat.insert(loads_nat.end(), c.tb_load_nat.begin(), c.tb_load_nat.end());
+    I.dev_stream_bytes += p.stream_bytes;
+    I.n_pages += p.n_pages;
+    I.dev_bytes += p.stream_bytes + (p.n_pages + 1) * 8 + (int64_t)(p.dev.grid + 1) * 4;
+    I.launches_per_spmv += p.n_pages > 0 ? 1 : 0;
+  }
+  I.alg_bytes += (int64_t)h->vec_size * (n + m);
+  load_stats(loads, &I.tb_load_mean, &I.tb_load_sd, &I.tb_load_max);
+  double mu_nat;
+  load_stats(loads_nat, &mu_nat, &I.tb_load_sd_natural, &I.tb_load_max_natural);
+  if (h->device >= 0) {
+    I.grid = h->parts[0].dev.grid;
+    if (m > 0) I.launches_per_spmv += 1;  // the y-zeroing kernel
+  } else {
+    I.launches_per_spmv = 0;
+  }
+  I.upload_seconds = t_up;
+  I.build_seconds = now() - t0 - t_up;
+  h->has_host = keep_host;
+  if (!h->has_host) {
+    for (Part &p : h->parts) {
+      cb::Canon small;
+      small.m = p.canon.m; small.n = p.canon.n; small.nnz = p.canon.nnz; small.nb = p.canon.nb;
+      small.T = p.canon.T; small.agg = p.canon.agg; small.blk_m = p.canon.blk_m;
+      p.canon = std::move(small);
+    }
+  }
+}
+
+static cbspmv_status_t build_impl(int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                                  const void *vals, cbspmv_dtype_t dtype, const cbspmv_options_t *opts, void *stream,
+                                  cbspmv_handle_t *out) {
   if (!out) return fail(CBSPMV_EINVAL, "null output handle pointer");
   *out = nullptr;
   cbspmv_options_t o;
@@ -185,7 +244,7 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
     if (opts->struct_size != sizeof(cbspmv_options_t)) return fail(CBSPMV_EINVAL, "options struct_size mismatch");
     o = *opts;
   }
-  if (dtype != CBSPMV_F64 && dtype != CBSPMV_F32) return fail(CBSPMV_EINVAL, "bad dtype");
+  if (!valid_dtype(dtype)) return fail(CBSPMV_EINVAL, "bad dtype");
   if (m < 0 || n < 0 || nnz < 0) return fail(CBSPMV_EINVAL, "negative dimension");
   if (m > 0 && !row_ptr) return fail(CBSPMV_EINVAL, "null row_ptr");
   if (o.device >= 0 && o.blk != 16) return fail(CBSPMV_EUNSUPPORTED, "device kernels require blk = 16");
@@ -196,7 +255,8 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
   cbspmv_s *h = new (std::nothrow) cbspmv_s();
   if (!h) return fail(CBSPMV_ENOMEM, "handle allocation");
   h->dtype = dtype;
-  h->val_size = dtype == CBSPMV_F64 ? 8 : 4;
+  h->val_size = val_bytes(dtype);
+  h->vec_size = vec_bytes(dtype);
   const int S = h->val_size;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (o.device >= 0) {
@@ -220,7 +280,7 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
     if (o.device >= 0) {
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, o.device);
-      const double xb = (double)n * S;
+      const double xb = (double)n * h->vec_size;
       if (l2 > 0 && xb > 0.75 * l2) P = (int)std::ceil(xb / (0.375 * l2));
     }
   }
@@ -234,7 +294,7 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
   h->parts.resize(P);
   if (P == 1) {
     h->parts[0].c0 = 0; h->parts[0].c1 = n;
-    st = build_part(A, o, cs, &h->parts[0], &t_up, &err);
+    st = build_part(A, o, dtype, cs, &h->parts[0], &t_up, &err);
   } else {
     int64_t nz = 0;
     st = cb::check_csr(A, o, &nz, &err);  // the split below relies on sorted, in-range columns
@@ -263,63 +323,33 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
       });
       cb::Csr Ak{m, n, snz, sub.rp.data(), sub.col.data(), sub.val.data(), S};
       h->parts[k].c0 = c0; h->parts[k].c1 = c1;
-      st = build_part(Ak, o, cs, &h->parts[k], &t_up, &err);
+      st = build_part(Ak, o, dtype, cs, &h->parts[k], &t_up, &err);
     }
   }
   if (st != CBSPMV_OK) { free_device(h); delete h; return fail(st, err); }
 
-  // info: sums over panels
-  cbspmv_info_t &I = h->info;
-  I.m = m; I.n = n; I.dtype = dtype; I.n_panels = P;
-  std::vector<int64_t> loads, loads_nat;
-  for (const Part &p : h->parts) {
-    const cb::Canon &c = p.canon;
-    I.nnz += c.nnz; I.nb += c.nb; I.nb_pre += c.nb_pre; I.ss_count += c.ss_count; I.agg |= c.agg;
-    I.blk_m = c.blk_m;
-    for (int k = 0; k < 3; k++) I.fmt_count[k] += c.fmt_count[k];
-    I.T += c.T;
-    I.mtx_bytes += (int64_t)c.mtx.size();
-    I.n_restore += (int64_t)c.restore.size();
-    I.meta_bytes += 21 * c.nb;
-    I.alg_bytes += 21 * c.nb + (int64_t)c.mtx.size() + 4 * (int64_t)c.restore.size() + (c.agg ? 8 * (c.blk_m + 1) : 0);
-    loads.insert(loads.end(), c.tb_load.begin(), c.tb_load.end());
-    loads_nat.insert(loads_nat.end(), c.tb_load_nat.begin(), c.tb_load_nat.end());
-    I.dev_stream_bytes += p.stream_bytes;
-    I.n_pages += p.n_pages;
-    I.dev_bytes += p.stream_bytes + (p.n_pages + 1) * 8 + (int64_t)(p.dev.grid + 1) * 4;
-    I.launches_per_spmv += p.n_pages > 0 ? 1 : 0;
-  }
-  I.alg_bytes += (int64_t)S * (n + m);
-  load_stats(loads, &I.tb_load_mean, &I.tb_load_sd, &I.tb_load_max);
-  double mu_nat;
-  load_stats(loads_nat, &mu_nat, &I.tb_load_sd_natural, &I.tb_load_max_natural);
-  if (h->device >= 0) {
-    I.grid = h->parts[0].dev.grid;
-    if (m > 0) I.launches_per_spmv += 1;  // the y-zeroing kernel
-  } else {
-    I.launches_per_spmv = 0;
-  }
-  I.upload_seconds = t_up;
-  I.build_seconds = now() - t0 - t_up;
-  h->has_host = o.keep_host != 0;
-  if (!h->has_host) {
-    for (Part &p : h->parts) {
-      cb::Canon small;
-      small.m = p.canon.m; small.n = p.canon.n; small.nnz = p.canon.nnz; small.nb = p.canon.nb;
-      small.T = p.canon.T; small.agg = p.canon.agg; small.blk_m = p.canon.blk_m;
-      p.canon = std::move(small);
-    }
-  }
+  fill_info(h, m, n, t0, t_up, o.keep_host != 0);
   *out = h;
   g_err.clear();
   return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                             const void *vals, cbspmv_dtype_t dtype, const cbspmv_options_t *opts, void *stream,
+                             cbspmv_handle_t *out) {
+  try {
+    return build_impl(m, n, nnz, row_ptr, col_idx, vals, dtype, opts, stream, out);
+  } catch (const std::bad_alloc &) {  // nothing throws across the ABI
+    if (out) *out = nullptr;
+    return fail(CBSPMV_ENOMEM, "host allocation during the build");
+  }
 }
 
 static cbspmv_status_t check_dev(cbspmv_handle_t h, const void *x, const void *y) {
   if (!h) return fail(CBSPMV_EINVAL, "null handle");
   if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle (built with device = -1)");
   if ((h->info.n > 0 && !x) || (h->info.m > 0 && !y)) return fail(CBSPMV_EINVAL, "null x or y");
-  const uintptr_t a = (uintptr_t)h->val_size - 1;
+  const uintptr_t a = (uintptr_t)h->vec_size - 1;
   if (((uintptr_t)x & a) || ((uintptr_t)y & a)) return fail(CBSPMV_EDIM, "x / y not aligned to the value size");
   if (x && y && x == y) return fail(CBSPMV_EINVAL, "y must not alias x");
   return CBSPMV_OK;
@@ -367,7 +397,7 @@ cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_
   if ((h->info.n > 0 && !x_host) || (h->info.m > 0 && !y_host)) return fail(CBSPMV_EINVAL, "null x or y");
   DeviceGuard g(h->device);
   cudaError_t e = cudaSuccess;
-  const size_t xb = (size_t)h->info.n * h->val_size, yb = (size_t)h->info.m * h->val_size;
+  const size_t xb = (size_t)h->info.n * h->vec_size, yb = (size_t)h->info.m * h->vec_size;
   if (!h->d_x_tmp && xb) e = cudaMalloc(&h->d_x_tmp, xb);
   if (e == cudaSuccess && !h->d_y_tmp && yb) e = cudaMalloc(&h->d_y_tmp, yb);
   if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ENOMEM, "device x/y staging"); }
@@ -386,6 +416,7 @@ cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_
 cbspmv_status_t cbspmv_sumsq(const void *v, int64_t len, cbspmv_dtype_t dtype, double *out, int32_t device,
                              void *stream) {
   if (!out || (len > 0 && !v) || len < 0) return fail(CBSPMV_EINVAL, "bad sumsq arguments");
+  if (!valid_dtype(dtype)) return fail(CBSPMV_EINVAL, "bad dtype");
   DeviceGuard g(device);
   std::string err;
   int st = cb_launch_sumsq(v, len, dtype, out, stream, &err);
@@ -403,9 +434,9 @@ cbspmv_status_t cbspmv_block_stats(int64_t m, int64_t n, int64_t nnz, const int6
     if (opts->struct_size != sizeof(cbspmv_options_t)) return fail(CBSPMV_EINVAL, "options struct_size mismatch");
     o = *opts;
   }
-  if (dtype != CBSPMV_F64 && dtype != CBSPMV_F32) return fail(CBSPMV_EINVAL, "bad dtype");
+  if (!valid_dtype(dtype)) return fail(CBSPMV_EINVAL, "bad dtype");
   if (m < 0 || n < 0 || nnz < 0 || (m > 0 && !row_ptr)) return fail(CBSPMV_EINVAL, "bad CSR");
-  cb::Csr A{m, n, nnz, row_ptr, col_idx, vals, dtype == CBSPMV_F64 ? 8 : 4};
+  cb::Csr A{m, n, nnz, row_ptr, col_idx, vals, val_bytes(dtype)};
   std::string err;
   int st = cb::block_stats(A, o, nb_pre, ss_count, &err);
   if (st != CBSPMV_OK) return fail(st, err);
@@ -472,6 +503,127 @@ cbspmv_status_t cbspmv_destroy(cbspmv_handle_t h) {
   return CBSPMV_OK;
 }
 
+// ------------------------------------------------------------------ files
+cbspmv_status_t cbspmv_mm_read(const char *path, cbspmv_csr_t *out) {
+  if (!path || !out) return fail(CBSPMV_EINVAL, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  try {
+    std::string err;
+    int st = cb::mm_read(path, 0, out, &err);
+    if (st != CBSPMV_OK) return fail(st, err);
+  } catch (const std::bad_alloc &) {
+    cbspmv_csr_free(out);
+    return fail(CBSPMV_ENOMEM, "host allocation while reading the file");
+  }
+  g_err.clear();
+  return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_mm_write(const char *path, int64_t m, int64_t n, const int64_t *row_ptr,
+                                const int32_t *col_idx, const double *vals) {
+  if (!path || m < 0 || n < 0 || (m > 0 && !row_ptr)) return fail(CBSPMV_EINVAL, "bad arguments");
+  if (m > 0 && row_ptr[m] > 0 && (!col_idx || !vals)) return fail(CBSPMV_EINVAL, "null col_idx / vals");
+  try {
+    std::string err;
+    int st = cb::mm_write(path, m, n, row_ptr, col_idx, vals, &err);
+    if (st != CBSPMV_OK) return fail(st, err);
+  } catch (const std::bad_alloc &) {
+    return fail(CBSPMV_ENOMEM, "host allocation while writing the file");
+  }
+  return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_csr_free(cbspmv_csr_t *csr) {
+  if (!csr) return CBSPMV_OK;
+  std::free(csr->row_ptr); std::free(csr->col_idx); std::free(csr->vals);
+  csr->row_ptr = nullptr; csr->col_idx = nullptr; csr->vals = nullptr;
+  csr->m = csr->n = csr->nnz = 0;
+  return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_save(cbspmv_handle_t h, const char *path) {
+  if (!h || !path) return fail(CBSPMV_EINVAL, "null argument");
+  if (!h->has_host) return fail(CBSPMV_EUNSUPPORTED, "built with keep_host = 0");
+  FILE *f = std::fopen(path, "wb");
+  if (!f) return fail(CBSPMV_EIO, std::string("cannot open ") + path + " for writing");
+  std::string err;
+  int st = CBSPMV_OK;
+  try {
+    for (size_t k = 0; k < h->parts.size() && st == CBSPMV_OK; k++) {
+      cb::CbsmExt x;
+      x.dtype = h->dtype; x.panel = (int)k; x.n_panels = (int)h->parts.size();
+      x.c0 = h->parts[k].c0; x.c1 = h->parts[k].c1;
+      st = cb::write_cbsm(f, h->parts[k].canon, x, &err);
+    }
+  } catch (const std::bad_alloc &) {
+    st = CBSPMV_ENOMEM; err = "host allocation while saving";
+  }
+  if (std::fclose(f) != 0 && st == CBSPMV_OK) { st = CBSPMV_EIO; err = "write failed"; }
+  if (st != CBSPMV_OK) { std::remove(path); return fail(st, err); }
+  return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_load(const char *path, const cbspmv_options_t *opts, void *stream, cbspmv_handle_t *out) {
+  if (!out || !path) return fail(CBSPMV_EINVAL, "null argument");
+  *out = nullptr;
+  cbspmv_options_t o;
+  cbspmv_default_options(&o);
+  if (opts) {
+    if (opts->struct_size != sizeof(cbspmv_options_t)) return fail(CBSPMV_EINVAL, "options struct_size mismatch");
+    o = *opts;
+  }
+  FILE *f = std::fopen(path, "rb");
+  if (!f) return fail(CBSPMV_EIO, std::string("cannot open ") + path);
+  cbspmv_s *h = new (std::nothrow) cbspmv_s();
+  if (!h) { std::fclose(f); return fail(CBSPMV_ENOMEM, "handle allocation"); }
+  std::string err;
+  int st = CBSPMV_OK;
+  const double t0 = now();
+  double t_up = 0.0;
+  int64_t m = 0, n = 0;
+  try {
+    if (o.device >= 0) {
+      int ndev = 0;
+      if (cudaGetDeviceCount(&ndev) != cudaSuccess || o.device >= ndev) {
+        cudaGetLastError();
+        st = CBSPMV_ECUDA; err = "no CUDA device " + std::to_string(o.device);
+      }
+      h->device = o.device;
+    }
+    DeviceGuard guard(st == CBSPMV_OK ? o.device : -1);
+    int n_panels = 1;
+    for (int k = 0; st == CBSPMV_OK && k < n_panels; k++) {
+      Part P;
+      cb::CbsmExt x;
+      st = cb::read_cbsm(f, &P.canon, &x, &err);
+      if (st != CBSPMV_OK) break;
+      if (k == 0) {
+        n_panels = x.n_panels; m = P.canon.m; n = P.canon.n;
+        h->dtype = x.dtype; h->val_size = val_bytes(x.dtype); h->vec_size = vec_bytes(x.dtype);
+      } else if (x.panel != k || x.n_panels != n_panels || x.dtype != h->dtype || P.canon.m != m || P.canon.n != n ||
+                 x.c0 != h->parts.back().c1) {
+        st = CBSPMV_EFORMAT; err = "inconsistent column panel " + std::to_string(k);
+        break;
+      }
+      if (x.panel != k) { st = CBSPMV_EFORMAT; err = "panel index out of order"; break; }
+      P.c0 = x.c0; P.c1 = x.c1;
+      h->parts.push_back(std::move(P));
+      if (o.device >= 0) st = upload_part(o, h->dtype, reinterpret_cast<cudaStream_t>(stream), &h->parts.back(), &t_up, &err);
+    }
+    if (st == CBSPMV_OK && (h->parts.empty() || h->parts.back().c1 != n || h->parts.front().c0 != 0)) {
+      st = CBSPMV_EFORMAT; err = "column panels do not cover [0, n)";
+    }
+  } catch (const std::bad_alloc &) {
+    st = CBSPMV_ENOMEM; err = "host allocation while loading";
+  }
+  std::fclose(f);
+  if (st != CBSPMV_OK) { free_device(h); delete h; return fail(st, err); }
+  fill_info(h, m, n, t0, t_up, o.keep_host != 0);
+  *out = h;
+  g_err.clear();
+  return CBSPMV_OK;
+}
+
 const char *cbspmv_status_string(cbspmv_status_t s) {
   switch (s) {
     case CBSPMV_OK: return "CBSPMV_OK";
@@ -481,6 +633,8 @@ const char *cbspmv_status_string(cbspmv_status_t s) {
     case CBSPMV_ECUDA: return "CBSPMV_ECUDA";
     case CBSPMV_EDIM: return "CBSPMV_EDIM";
     case CBSPMV_EUNSUPPORTED: return "CBSPMV_EUNSUPPORTED";
+    case CBSPMV_EIO: return "CBSPMV_EIO";
+    case CBSPMV_EFORMAT: return "CBSPMV_EFORMAT";
   }
   return "unknown status";
 }

@@ -2,6 +2,7 @@
 // Product path only; nothing here is shared with oracle/.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <functional>
 #include <memory>
 #include <utility>
@@ -110,8 +111,24 @@ struct Stream {
   int64_t nbytes = 0;
   std::vector<uint64_t> page_off;  // n_pages + 1
 };
-int build_stream(const Canon &c, int page_cap, int threads, Stream *s, std::string *err);
+// x_size: bytes of one x element (sizes the non-aggregated x tiles that follow each page)
+int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, std::string *err);
 void free_stream(Stream *s);
+
+// Matrix Market coordinate files (mmio.cpp)
+int mm_read(const char *path, int threads, cbspmv_csr_t *out, std::string *err);
+int mm_write(const char *path, int64_t m, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+             const double *vals, std::string *err);
+
+// CBSM container (container.cpp) + this library's extension block
+struct CbsmExt {
+  int dtype = CBSPMV_F64;
+  int panel = 0, n_panels = 1;
+  int64_t c0 = 0, c1 = 0;  // the panel's columns [c0, c1)
+};
+int write_cbsm(FILE *f, const Canon &c, const CbsmExt &x, std::string *err);
+int read_cbsm(FILE *f, Canon *out, CbsmExt *x, std::string *err);  // validates (validate_canon)
+int validate_canon(const Canon &c, const CbsmExt &x, std::string *err);
 
 // Threads
 void parallel_for(int64_t n, int threads, int64_t grain, const std::function<void(int64_t, int64_t, int)> &fn);

@@ -155,7 +155,7 @@ struct CooPend {
   bool valid;
 };
 
-template <typename V, bool AGG>
+template <typename M, typename V, bool AGG>
 __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4 *descs, uint32_t iw,
                                                 const V *xbuf, const V *__restrict__ x, int lane, Dbg dbg,
                                                 uint64_t xpol) {
@@ -169,11 +169,11 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   const int i = lane - lane0;
   r.valid = i < d_nnz(d);
   const uint8_t *body = page + (d.z & 0xFFFFu);
-  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const M *vals = reinterpret_cast<const M *>(page + (d.z >> 16));
   const uint32_t byte = r.valid ? body[i] : 0u;
   const int col = byte >> 4;
   r.yrow = d.x + (byte & 15);
-  r.v = r.valid ? vals[i] : V(0);
+  r.v = r.valid ? V(vals[i]) : V(0);
   r.xv = V(0);
   if (r.valid) {
     if constexpr (AGG) {
@@ -212,15 +212,15 @@ __device__ __forceinline__ const V *warp_tile(const uint8_t *page, const uint4 &
 }
 
 // A COO block too large for a group (forced format): chunks of 32 elements.
-template <typename V, bool SCALED>
+template <typename M, typename V, bool SCALED>
 __device__ __forceinline__ void coo_big(const uint8_t *page, const uint4 &d, const V *xt, V scale,
                                         V *__restrict__ y, int lane, Dbg dbg) {
   const uint8_t *body = page + (d.z & 0xFFFFu);
-  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const M *vals = reinterpret_cast<const M *>(page + (d.z >> 16));
   const int nnz = d_nnz(d);
   for (int e = lane; e < nnz; e += 32) {
     const uint32_t byte = body[e];
-    V p = vals[e] * xt[byte >> 4];
+    V p = V(vals[e]) * xt[byte >> 4];
     if constexpr (SCALED) p *= scale;
     red_add(y + d.x + (byte & 15), p, dbg);
   }
@@ -228,18 +228,18 @@ __device__ __forceinline__ void coo_big(const uint8_t *page, const uint4 &d, con
 
 // CSR: 17 u8 row_ptr, nnz u8 local cols, pad, values; lanes 2r, 2r+1 share row r
 // ("32 threads collaboratively compute 16 y elements").
-template <typename V, bool SCALED>
+template <typename M, typename V, bool SCALED>
 __device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, const V *xt, V scale,
                                          V *__restrict__ y, int lane, Dbg dbg) {
   const uint8_t *body = page + (d.z & 0xFFFFu);
   const uint8_t *cols = body + 17;
-  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const M *vals = reinterpret_cast<const M *>(page + (d.z >> 16));
   const int nnz = d_nnz(d);
   const int r = lane >> 1, h = lane & 1;
   const int lo = body[r];
   const int hi = r < 15 ? (int)body[r + 1] : nnz;  // row_ptr[16] = nnz (R-8)
   V acc = V(0);
-  for (int e = lo + h; e < hi; e += 2) acc = fma(vals[e], xt[cols[e]], acc);
+  for (int e = lo + h; e < hi; e += 2) acc = fma(V(vals[e]), xt[cols[e]], acc);
   acc += __shfl_xor_sync(kFull, acc, 1);
   if constexpr (SCALED) acc *= scale;
   if (h == 0 && hi > lo) red_add(y + d.x + r, acc, dbg);
@@ -249,27 +249,27 @@ __device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, co
 // k*32 + lane holds A[lane % 16][(lane / 16) * 8 + k], so lane l owns row l % 16, columns
 // 8*(l/16) .. +7 — conflict-free 8-byte shared loads, 8 FMAs against the broadcast x tile, one
 // shfl_xor(16) joins the two half rows (the semantics of Alg. 4's shfl, R-15), 16 REDs.
-template <typename V, bool SCALED>
+template <typename M, typename V, bool SCALED>
 __device__ __forceinline__ void dense_path(const uint8_t *page, const uint4 &d, const V *xt, V scale,
                                            V *__restrict__ y, int64_t m, int lane, Dbg dbg) {
-  const V *vals = reinterpret_cast<const V *>(page + (d.z >> 16));
+  const M *vals = reinterpret_cast<const M *>(page + (d.z >> 16));
   const int h = lane >> 4, r = lane & 15, nc = d_ncols(d);
   // absent entries (stored zeros) must contribute 0 even against non-finite x: check the tile once
   const bool finite = __all_sync(kFull, r >= nc || isfinite(xt[r]));
   V acc = V(0);
   if (finite && nc == 16) {  // full tile (every block column but a ragged last one)
 #pragma unroll
-    for (int k = 0; k < 8; k++) acc = fma(vals[k * 32 + lane], xt[h * 8 + k], acc);
+    for (int k = 0; k < 8; k++) acc = fma(V(vals[k * 32 + lane]), xt[h * 8 + k], acc);
   } else if (finite) {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const int c = h * 8 + k;
-      acc = fma(vals[k * 32 + lane], c < nc ? xt[c] : V(0), acc);
+      acc = fma(V(vals[k * 32 + lane]), c < nc ? xt[c] : V(0), acc);
     }
   } else {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      const V v = vals[k * 32 + lane];
+      const V v = V(vals[k * 32 + lane]);
       const int c = h * 8 + k;
       if (v != V(0)) acc = fma(v, xt[c], acc);
     }
@@ -318,8 +318,9 @@ __device__ __forceinline__ void issue_tiles(const uint4 *descs, uint32_t iw, V *
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// Warp roles: 0 = TMA producer, the rest = consumer groups.
-template <typename V, bool AGG, bool SCALED>
+// Warp roles: 0 = TMA producer, the rest = consumer groups.  M: matrix value type of the
+// records; V: type of x, y and the accumulation (M = float, V = double: the mixed variant).
+template <typename M, typename V, bool AGG, bool SCALED>
 __global__ void __launch_bounds__(kMaxThreads, 1)
     cb_spmv_kernel(KParams P, const V *__restrict__ x, V *__restrict__ y) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         if (all_coo) {
           CooPend<V> q[4];
 #pragma unroll
-          for (int j = 0; j < 4; j++) q[j] = coo_issue<V, AGG>(page, descs, iws[j], xbuf, x, lane, dbg, xpol);
+          for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V, AGG>(page, descs, iws[j], xbuf, x, lane, dbg, xpol);
 #pragma unroll
           for (int j = 0; j < 4; j++) coo_finish<V, SCALED>(q[j], scale, y, dbg);
         } else {
@@ -414,13 +415,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             const uint32_t iw = iws[j];
             const int t = (iw >> 12) & 3;
             if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
-              coo_finish<V, SCALED>(coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
+              coo_finish<V, SCALED>(coo_issue<M, V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
             } else {
               const uint4 dh = descs[iw & 0xFFF];
               const V *xt = warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg);
-              if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
-              else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
-              else dense_path<V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
+              if (t == CBSPMV_FMT_COO) coo_big<M, V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+              else if (t == CBSPMV_FMT_CSR) csr_path<M, V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+              else dense_path<M, V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
               __syncwarp();
             }
           }
@@ -445,13 +446,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         __syncwarp();
         const int t = (iw >> 12) & 3, hb = iw & 0xFFF;
         if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
-          coo_finish<V, SCALED>(coo_issue<V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
+          coo_finish<V, SCALED>(coo_issue<M, V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
         } else {
           const uint4 dh = descs[hb];
           const V *xt = xbuf + hb * 16;
-          if (t == CBSPMV_FMT_COO) coo_big<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
-          else if (t == CBSPMV_FMT_CSR) csr_path<V, SCALED>(page, dh, xt, scale, y, lane, dbg);
-          else dense_path<V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
+          if (t == CBSPMV_FMT_COO) coo_big<M, V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+          else if (t == CBSPMV_FMT_CSR) csr_path<M, V, SCALED>(page, dh, xt, scale, y, lane, dbg);
+          else dense_path<M, V, SCALED>(page, dh, xt, scale, y, P.m, lane, dbg);
         }
         k = kn;
         iw = iwn;
@@ -491,21 +492,20 @@ __global__ void cb_sumsq_kernel(const V *__restrict__ v, int64_t len, double *ou
   }
 }
 
-using KFn = void (*)(KParams, const void *, void *);
-
-template <typename V, bool AGG, bool SCALED>
-const void *kernel_ptr() {
-  return reinterpret_cast<const void *>(&cb_spmv_kernel<V, AGG, SCALED>);
+template <typename M, typename V>
+const void *kernel_ptr(int agg, bool scaled) {
+  if (agg) return scaled ? (const void *)&cb_spmv_kernel<M, V, true, true> : (const void *)&cb_spmv_kernel<M, V, true, false>;
+  return scaled ? (const void *)&cb_spmv_kernel<M, V, false, true> : (const void *)&cb_spmv_kernel<M, V, false, false>;
 }
 
 const void *select_kernel(int dtype, int agg, bool scaled) {
-  if (dtype == CBSPMV_F64) {
-    if (agg) return scaled ? kernel_ptr<double, true, true>() : kernel_ptr<double, true, false>();
-    return scaled ? kernel_ptr<double, false, true>() : kernel_ptr<double, false, false>();
-  }
-  if (agg) return scaled ? kernel_ptr<float, true, true>() : kernel_ptr<float, true, false>();
-  return scaled ? kernel_ptr<float, false, true>() : kernel_ptr<float, false, false>();
+  if (dtype == CBSPMV_F64) return kernel_ptr<double, double>(agg, scaled);
+  if (dtype == CBSPMV_F32) return kernel_ptr<float, float>(agg, scaled);
+  return kernel_ptr<float, double>(agg, scaled);  // CBSPMV_F32F64
 }
+
+// bytes of one x / y element
+inline int vec_bytes(int dtype) { return dtype == CBSPMV_F32 ? 4 : 8; }
 
 inline int cuda_fail(cudaError_t e, const char *what, std::string *err) {
   *err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -535,7 +535,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
   int groups = genv ? std::atoi(genv) : 5;
   groups = std::max(1, std::min(kMaxGroups, groups));
   dev->groups = groups;
-  const int header = kSmemHeader + groups * kGroupWarps * 16 * (dev->dtype == CBSPMV_F64 ? 8 : 4);
+  const int header = kSmemHeader + groups * kGroupWarps * 16 * vec_bytes(dev->dtype);
   const int stage = dev->page_cap;
   const int budget = std::min(optin, smem_sm / ctas - 1024);  // 1 KB per CTA is reserved by the system
   int nstage = (budget - header) / stage;
@@ -546,7 +546,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
   }
   dev->nstage = nstage;
   dev->consumers = groups * kGroupWarps;
-  for (int dt = 0; dt < 2; dt++)
+  for (int dt = 0; dt < 3; dt++)
     for (int agg = 0; agg < 2; agg++)
       for (int sc = 0; sc < 2; sc++) {
         e = cudaFuncSetAttribute(select_kernel(dt, agg, sc), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
@@ -566,7 +566,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     const int zb = 256;
     int64_t need = (dev.m + zb - 1) / zb;
     int zg = (int)(need < (int64_t)sms * 8 ? need : (int64_t)sms * 8);
-    if (dev.dtype == CBSPMV_F64) cb_zero_kernel<double><<<zg, zb, 0, st>>>((double *)y, dev.m);
+    if (vec_bytes(dev.dtype) == 8) cb_zero_kernel<double><<<zg, zb, 0, st>>>((double *)y, dev.m);
     else cb_zero_kernel<float><<<zg, zb, 0, st>>>((float *)y, dev.m);
   }
   static const int dbg_skip = [] {
@@ -578,7 +578,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     const int vec16 = !dev.agg && ((uintptr_t)x % 16 == 0);
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, dev.groups,
               vec16, Dbg{dbg_skip}};
-    const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * (dev.dtype == CBSPMV_F64 ? 8 : 4);
+    const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * vec_bytes(dev.dtype);
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
     const int threads = 32 * (1 + dev.groups * kGroupWarps);
@@ -600,7 +600,7 @@ int cb_launch_sumsq(const void *v, int64_t len, int dtype, double *out, void *st
     const int sms = sm_count(dev);
     int64_t need = (len + 255) / 256;
     int g = (int)(need < (int64_t)sms * 4 ? need : (int64_t)sms * 4);
-    if (dtype == CBSPMV_F64) cb_sumsq_kernel<double><<<g, 256, 0, st>>>((const double *)v, len, out);
+    if (vec_bytes(dtype) == 8) cb_sumsq_kernel<double><<<g, 256, 0, st>>>((const double *)v, len, out);
     else cb_sumsq_kernel<float><<<g, 256, 0, st>>>((const float *)v, len, out);
   }
   e = cudaGetLastError();

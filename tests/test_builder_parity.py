@@ -59,6 +59,8 @@ def test_warps_per_tb(A, W):
 def test_fp32(A):
     compare(A, dtype="f32")
     compare(A, dtype="f32", agg_mode=1)
+    info = compare(A, dtype="f32f64")  # mixed variant (R-24): the fp32 record layout
+    assert info["dtype"] == cb.F32F64
 
 
 def test_fig1_blk4():

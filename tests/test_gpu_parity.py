@@ -28,7 +28,7 @@ def _ok():
 
 def gpu_spmv(A, x, dtype="f64", **opts):
     _ok()
-    tdt = torch.float64 if dtype == "f64" else torch.float32
+    tdt = torch.float32 if dtype == "f32" else torch.float64
     h = cb.build(A, dtype=dtype, device=0, **opts)
     xd = torch.from_numpy(np.ascontiguousarray(x)).to(DEV, tdt)
     yd = torch.full((A.m,), float("nan"), dtype=tdt, device=DEV)  # spmv must overwrite every row
@@ -50,6 +50,12 @@ def check_rows(y, y_ref, R, rel):
 def ref32(A, x):
     A32 = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
     return oracle.spmv_csr(A32, x.astype(np.float32).astype(np.float64))
+
+
+def refmix(A, x):
+    """Mixed variant (R-24): the fp64 product of the fp32-rounded matrix with the fp64 x."""
+    A32 = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
+    return oracle.spmv_csr(A32, x)
 
 
 # ----------------------------------------------------------------------------- corpus, every variant
@@ -82,8 +88,19 @@ def test_corpus_fp32(A, agg, ff):
     check_rows(y, y_ref, R, 1e-5)
 
 
+@pytest.mark.parametrize("A", CORPUS[::2], ids=lambda A: A.name)
+@pytest.mark.parametrize("agg", [0, 1])
+@pytest.mark.parametrize("ff", [-1, 0, 1, 2])
+def test_corpus_mixed_f32_values_f64_accumulation(A, agg, ff):
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=10)
+    y_ref, R = refmix(A, x)
+    y, h = gpu_spmv(A, x, dtype="f32f64", agg_mode=agg, force_format=ff)
+    assert h.info["dtype"] == cb.F32F64
+    check_rows(y, y_ref, R, 1e-12)
+
+
 @pytest.mark.parametrize("pattern", ["random", "hub", "blockdense", "banded"])
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("dtype", ["f64", "f32", "f32f64"])
 @pytest.mark.parametrize("agg", [0, 1])
 def test_exact_integer_mode_bitwise(pattern, dtype, agg):
     A = synth.random_csr(300, 260, 0.08, 17, val_mode=2, pattern=pattern)
@@ -202,16 +219,17 @@ def decode_stream(stream, page_off):
 
 
 @pytest.mark.parametrize("name", ["laplace", "rmat", "clustered"])
-def test_device_stream_encodes_canonical_format(name):
+@pytest.mark.parametrize("dtype", ["f64", "f32f64"])
+def test_device_stream_encodes_canonical_format(name, dtype):
     """What is on the device is exactly the canonical format (slot order), records byte-equal."""
     _ok()
     A = synth.make(name, small=True)
-    h = cb.build(A, device=0)
+    h = cb.build(A, dtype=dtype, device=0)
     ex = cb.export(h)
     s, po = cb.download_stream(h)
     blocks = decode_stream(s, po)
     assert len(blocks) == ex["nb"]
-    S = 8
+    S = 8 if dtype == "f64" else 4
     agg = h.info["agg"]
     for i, b in enumerate(blocks):
         br, bc = int(ex["blk_row_idx"][i]), int(ex["blk_col_idx"][i])
@@ -243,19 +261,20 @@ def test_device_stream_encodes_canonical_format(name):
         if typ == 2:  # lane-major dense layout: slot k*32 + l holds A[l % 16][(l // 16) * 8 + k]
             k, l = np.divmod(np.arange(256), 32)
             src = (l % 16) * 16 + (l // 16) * 8 + k
-            dev_rec = dev_rec.view(np.float64)[np.argsort(src)].view(np.uint8)
+            dev_rec = dev_rec.view(np.float64 if S == 8 else np.float32)[np.argsort(src)].view(np.uint8)
         assert np.array_equal(dev_rec, ex["mtx_data"][vp:vp + size])
 
 
 # ----------------------------------------------------------------------------- BASELINE configs
 @pytest.mark.parametrize("name", ["laplace", "rmat", "clustered", "uniform"])
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("dtype", ["f64", "f32", "f32f64"])
 def test_configs_small_full_check(name, dtype):
     A = synth.make(name, small=True)
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=12)
-    y_ref, R = oracle.spmv_csr(A, x) if dtype == "f64" else ref32(A, x)
+    ref = {"f64": oracle.spmv_csr, "f32": ref32, "f32f64": refmix}[dtype]
+    y_ref, R = ref(A, x)
     y, h = gpu_spmv(A, x, dtype=dtype)
-    check_rows(y, y_ref, R, 1e-12 if dtype == "f64" else 1e-5)
+    check_rows(y, y_ref, R, 1e-5 if dtype == "f32" else 1e-12)
 
 
 def test_laplace_config2_full():
@@ -294,7 +313,7 @@ def test_rmat_config3_full_sampled():
     assert np.all(np.abs(y1 - sums) <= 1e-12 * rs)
 
 
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("dtype", ["f64", "f32", "f32f64"])
 def test_clustered_config4_full_sampled(dtype):
     A = synth.make("clustered")
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=42)
@@ -302,6 +321,8 @@ def test_clustered_config4_full_sampled(dtype):
     assert h.info["agg"] == 0 and min(h.info["fmt_count"]) > 0
     if dtype == "f64":
         sampled(A, y, x, 1e-12)
+    elif dtype == "f32f64":
+        sampled(synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64)), y, x, 1e-12)
     else:
         rows = np.sort(np.random.default_rng(1).choice(A.m, size=20000, replace=False))
         A32 = synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
@@ -382,6 +403,26 @@ def test_column_panels_spmv(P, name):
     y_ref, R = oracle.spmv_csr(A, x)
     y, h = gpu_spmv(A, x, col_panels=P)
     assert h.info["n_panels"] == P
+    check_rows(y, y_ref, R, 1e-12)
+    xd = torch.from_numpy(x).to(DEV)
+    ss = torch.tensor([4.0], dtype=torch.float64, device=DEV)
+    ys = torch.empty(A.m, dtype=torch.float64, device=DEV)
+    cb.spmv_scaled(h, xd, ss, ys)
+    torch.cuda.synchronize()
+    check_rows(ys.cpu().numpy() * 2.0, y_ref, R, 1e-12)
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_mixed_host_scaled_and_panels(P):
+    """Mixed variant through spmv_host (fp64 host buffers), spmv_scaled and column panels."""
+    _ok()
+    A = synth.make("rmat", small=True)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=13)
+    y_ref, R = refmix(A, x)
+    h = cb.build(A, dtype="f32f64", device=0, col_panels=P)
+    assert h.info["n_panels"] == P
+    y = np.empty(A.m)
+    cb.spmv_host(h, x, y)
     check_rows(y, y_ref, R, 1e-12)
     xd = torch.from_numpy(x).to(DEV)
     ss = torch.tensor([4.0], dtype=torch.float64, device=DEV)
