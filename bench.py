@@ -377,11 +377,20 @@ def run_power(args, rank, world, local_rank):
     A, (r0, r1), nnz_total = make_matrix("uniform", rank, world)
     gen_s = time.perf_counter() - t0
     agg = dist.global_agg(A, lambda a: _allreduce_np(a, dev, world), dtype=args.dtype) if world > 1 else -1
-    h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0)
+    # column panels: the auto count on one GPU (x slices L2-resident); with N ranks a multiple
+    # of N so panel cuts fall on the x owners' boundaries (NEXT-1 (i) overlap)
+    panels = 0 if world == 1 else world * max(1, -(-6 // world))
+    h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0, col_panels=panels)
     info = h.info
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     x0 = torch.ones(A.n, dtype=tdt, device=dev)
-    dist.power_iteration_device(h, x0, max(args.warmup, 3), world)
+    if args.no_overlap:
+        def run_steps(n):
+            return dist.power_iteration_device(h, x0, n, world)
+    else:
+        def run_steps(n):
+            return dist.power_iteration_overlapped(h, x0, n, world, rank)
+    run_steps(max(args.warmup, 3))
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
@@ -389,7 +398,7 @@ def run_power(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         e0.record(st)
-        x, ss = dist.power_iteration_device(h, x0, args.steps, world)
+        x, ss = run_steps(args.steps)
         e1.record(st)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -412,12 +421,14 @@ def run_power(args, rank, world, local_rank):
             "config": {"workload": "BASELINE configs[4]: power iteration on uniform 2^25 x 2^25, 50 nnz/row",
                        "name": "uniform", "nnz": int(nnz_total), "rows_per_rank": int(A.m), "agg": int(info["agg"]),
                        "lambda": lam, "gen_s": gen_s, "build_s": info["build_seconds"],
-                       "parallelism": f"row-shard x{world}, NCCL all-reduce + all-gather per step"},
+                       "n_panels": int(info["n_panels"]),
+                       "parallelism": f"row-shard x{world}, " + ("NCCL all-reduce + all-gather per step" if args.no_overlap
+                                      else "NCCL all-reduce + per-owner broadcasts overlapped with column panels")},
             "roofline": {"bound": "hbm", "achieved": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9 / peak,
                          "traffic": ncu_traffic("uniform", args.dtype), "kernel": "cb_spmv_kernel",
                          "kernel_ms": kernel_ms, "peak_source": peak_src},
-            "gpu_launches": int(args.steps * (2 + 1)),
+            "gpu_launches": int(args.steps * (2 + (1 if args.no_overlap else info["n_panels"]))),
             "clocks": clk.summary(), "cpu_baseline": None,
             "e2e": None,
         }
@@ -478,6 +489,8 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32", "f32f64"])
     ap.add_argument("--impl", default="cb", choices=["cb", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="uniform power iteration: plain all-gather instead of per-owner broadcasts + panels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

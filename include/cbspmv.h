@@ -159,6 +159,17 @@ cbspmv_status_t cbspmv_spmv_add(cbspmv_handle_t h, const void *x_dev, void *y_de
 cbspmv_status_t cbspmv_spmv_scaled(cbspmv_handle_t h, const void *x_dev, const double *sumsq_dev,
                                    void *y_dev, void *stream);
 
+/* One column panel k (0 <= k < info.n_panels) alone: y (+)= A[:, c_k:c_k+1) · (s·x) with
+ * s = 1/sqrt(*sumsq_dev), or s = 1 when sumsq_dev is NULL; zero_y != 0 zeroes y first.  Only
+ * x[c_k, c_k+1) is read, so a caller whose x arrives slice by slice (the all-gather of power
+ * iteration) can run panel k as soon as its slice is present.  Running
+ * every panel once, the first with zero_y, equals cbspmv_spmv / cbspmv_spmv_scaled. */
+cbspmv_status_t cbspmv_spmv_panel(cbspmv_handle_t h, int32_t k, const void *x_dev, const double *sumsq_dev,
+                                  void *y_dev, int32_t zero_y, void *stream);
+
+/* Columns [*c0, *c1) of panel k. */
+cbspmv_status_t cbspmv_panel_bounds(cbspmv_handle_t h, int32_t k, int64_t *c0, int64_t *c1);
+
 /* End to end with host buffers: copies x_host (n values) to the device, runs
  * cbspmv_spmv into an internal device y, copies y back to y_host (m values),
  * and synchronises the stream before returning. */

@@ -103,6 +103,8 @@ def lib():
             "cbspmv_spmv_add": ([H, vp, vp, vp], i32),
             "cbspmv_spmv_scaled": ([H, vp, vp, vp, vp], i32),
             "cbspmv_spmv_host": ([H, vp, vp, vp], i32),
+            "cbspmv_spmv_panel": ([H, i32, vp, vp, vp, i32, vp], i32),
+            "cbspmv_panel_bounds": ([H, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
             "cbspmv_sumsq": ([vp, i64, i32, vp, i32, vp], i32),
             "cbspmv_block_stats": ([i64, i64, i64, vp, vp, vp, i32, ctypes.POINTER(Options),
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
@@ -254,6 +256,18 @@ def spmv_add(h: Handle, x, y, stream=None) -> None:
 def spmv_scaled(h: Handle, x, sumsq_dev, y, stream=None) -> None:
     _check(lib().cbspmv_spmv_scaled(h.raw, _ptr(x), _ptr(sumsq_dev), _ptr(y), _stream(stream, h.device)),
            "cbspmv_spmv_scaled")
+
+
+def spmv_panel(h: Handle, k: int, x, sumsq_dev, y, zero_y: bool, stream=None) -> None:
+    """cbspmv_spmv_panel: column panel k only, y (+)= A[:, panel k] (s x); sumsq_dev None -> s = 1."""
+    _check(lib().cbspmv_spmv_panel(h.raw, int(k), _ptr(x), _ptr(sumsq_dev), _ptr(y), int(bool(zero_y)),
+                                   _stream(stream, h.device)), "cbspmv_spmv_panel")
+
+
+def panel_bounds(h: Handle, k: int) -> tuple[int, int]:
+    c0, c1 = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().cbspmv_panel_bounds(h.raw, int(k), ctypes.byref(c0), ctypes.byref(c1)), "cbspmv_panel_bounds")
+    return c0.value, c1.value
 
 
 def spmv_host(h: Handle, x: np.ndarray, y: np.ndarray, stream=None) -> None:

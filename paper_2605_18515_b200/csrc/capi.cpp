@@ -391,6 +391,26 @@ cbspmv_status_t cbspmv_spmv_scaled(cbspmv_handle_t h, const void *x, const doubl
   return run(h, x, y, sumsq, true, stream);
 }
 
+cbspmv_status_t cbspmv_spmv_panel(cbspmv_handle_t h, int32_t k, const void *x, const double *sumsq, void *y,
+                                  int32_t zero_y, void *stream) {
+  cbspmv_status_t s = check_dev(h, x, y);
+  if (s != CBSPMV_OK) return s;
+  if (k < 0 || k >= (int32_t)h->parts.size()) return fail(CBSPMV_EINVAL, "panel index out of range");
+  DeviceGuard g(h->device);
+  std::string err;
+  int st = cb_launch_spmv(h->parts[k].dev, x, y, sumsq, zero_y != 0, stream, &err);
+  if (st != CBSPMV_OK) return fail(st, err);
+  return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_panel_bounds(cbspmv_handle_t h, int32_t k, int64_t *c0, int64_t *c1) {
+  if (!h || !c0 || !c1) return fail(CBSPMV_EINVAL, "null argument");
+  if (k < 0 || k >= (int32_t)h->parts.size()) return fail(CBSPMV_EINVAL, "panel index out of range");
+  *c0 = h->parts[k].c0;
+  *c1 = h->parts[k].c1;
+  return CBSPMV_OK;
+}
+
 cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_host, void *stream) {
   if (!h) return fail(CBSPMV_EINVAL, "null handle");
   if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle");

@@ -14,6 +14,11 @@
   by ``cbspmv_spmv_scaled``), then sum(y_k^2) all-reduced and y shards all-gathered
   into the next x over NCCL.
 
+* ``PanelPowerIteration`` / ``power_iteration_overlapped``:
+  the same recurrence with the all-gather split into one broadcast per x owner and
+  the next step's column panels (``cbspmv_spmv_panel``) each started as soon as the
+  x slices it reads have arrived, so the exchange hides behind the SpMV.
+
 Collectives go through ``torch.distributed`` (NCCL on GPUs, gloo in CPU tests);
 the compute steps are injected so the host logic is testable without a GPU.
 """
@@ -117,3 +122,94 @@ def power_iteration_device(h, x0, steps: int, world: int = 1, group=None, on_ste
         if on_step is not None:
             on_step(k, x, ss)
     return x, ss
+
+
+def panel_owners(c0: int, c1: int, row_bounds) -> list[int]:
+    """Ranks whose x slice [r_a, r_b) intersects the panel's columns [c0, c1)."""
+    return [r for r, (a, b) in enumerate(row_bounds) if a < c1 and b > c0]
+
+
+class PanelPowerIteration:
+    """NEXT-1 (i): power iteration whose x exchange overlaps the next step's SpMV.
+
+    Same recurrence as ``PowerIteration`` (y_k = A_shard (x_k / sqrt(sumsq_{k-1})),
+    sumsq_k = allreduce(sum y_k^2), x_{k+1} = concat of the y_k shards).  x is double-buffered:
+    y_k is computed in place into the next buffer's own slice, then every rank broadcasts its
+    slice (one asynchronous collective per owner, issued in owner order, identical on every
+    rank).  Step k+1 runs its column panels in arrival order -- panels reading only the rank's
+    own slice first -- and waits, before each panel, on exactly the broadcasts that panel reads;
+    all of a step's broadcasts are waited before the step ends, so no buffer is overwritten
+    while a broadcast still reads it.
+
+    Injected ops (device: the C ABI + NCCL, ``power_iteration_overlapped``; CPU tests: numpy +
+    gloo): ``spmv_panel(p, x, sumsq, y, zero_y)``, ``sumsq_fn(y, out)``,
+    ``all_reduce_sum_async(t) -> work``, ``broadcast_async(t, src) -> work``; ``work.wait()``
+    orders the caller after the collective.  ``panels``: column bounds of the handle's panels;
+    ``row_bounds``: the x slice each rank owns (its y rows)."""
+
+    def __init__(self, spmv_panel, sumsq_fn, all_reduce_sum_async, broadcast_async, panels, row_bounds, rank):
+        self.spmv_panel, self.sumsq_fn = spmv_panel, sumsq_fn
+        self.all_reduce_sum_async, self.broadcast_async = all_reduce_sum_async, broadcast_async
+        self.row_bounds = [(int(a), int(b)) for a, b in row_bounds]
+        self.rank = rank
+        self.owners = [panel_owners(c0, c1, self.row_bounds) for c0, c1 in panels]
+        remote = [max([o for o in ow if o != rank], default=-1) for ow in self.owners]
+        self.order = sorted(range(len(panels)), key=lambda p: (remote[p], p))
+
+    def run(self, xa, xb, sumsq, steps: int, on_step=None):
+        """xa: full x_0 (replicated), xb: a second full-length buffer, sumsq: sum(x_0^2).
+        Returns (x, sumsq) with x = the last iterate (complete on return)."""
+        world = len(self.row_bounds)
+        r0, r1 = self.row_bounds[self.rank]
+        pending = {}
+        cur, nxt = xa, xb
+        for k in range(steps):
+            y = nxt[r0:r1]
+            for i, p in enumerate(self.order):
+                for o in self.owners[p]:
+                    w = pending.pop(o, None)
+                    if w is not None:
+                        w.wait()
+                self.spmv_panel(p, cur, sumsq, y, i == 0)
+            for w in pending.values():  # incl. this rank's own (source) broadcast
+                w.wait()
+            pending = {}
+            self.sumsq_fn(y, sumsq)
+            if world > 1:
+                self.all_reduce_sum_async(sumsq).wait()
+                pending = {s: self.broadcast_async(nxt[a:b], s) for s, (a, b) in enumerate(self.row_bounds)}
+            cur, nxt = nxt, cur
+            if on_step is not None:  # debugging / tests: a complete x costs the overlap
+                for w in pending.values():
+                    w.wait()
+                pending = {}
+                on_step(k, cur, sumsq)
+        for w in pending.values():
+            w.wait()
+        return cur, sumsq
+
+
+def power_iteration_overlapped(h, x0, steps: int, world: int = 1, rank: int = 0, group=None, on_step=None):
+    """``PanelPowerIteration`` on the device: panels through ``cbspmv_spmv_panel``, the
+    finalize through ``cbspmv_sumsq``, collectives over NCCL (``async_op`` works whose
+    ``wait()`` makes the current stream wait, not the host).  Equal row shards of a square
+    matrix; x0 is the full start vector.  Returns (x, sumsq) on the device."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2605_18515_b200 as cb
+    m_local = h.info["m"]
+    dev = x0.device.index
+    row_bounds = [(r * m_local, (r + 1) * m_local) for r in range(world)]
+    panels = [cb.panel_bounds(h, p) for p in range(h.info["n_panels"])]
+    it = PanelPowerIteration(
+        spmv_panel=lambda p, x, ss, y, z: cb.spmv_panel(h, p, x, ss, y, z),
+        sumsq_fn=lambda y, out: cb.sumsq(y, out, device=dev),
+        all_reduce_sum_async=lambda t: tdist.all_reduce(t, group=group, async_op=True),
+        broadcast_async=lambda t, src: tdist.broadcast(t, src=src, group=group, async_op=True),
+        panels=panels, row_bounds=row_bounds, rank=rank)
+    xa = x0.clone()
+    xb = torch.empty_like(x0)
+    ss = torch.zeros(1, dtype=torch.float64, device=x0.device)
+    cb.sumsq(xa, ss, device=dev)
+    return it.run(xa, xb, ss, steps, on_step=on_step)

@@ -157,3 +157,82 @@ def test_two_rank_power_iteration_matches_single_process():
     # Perron root of a nonnegative matrix with row sums in [?]: bounded by min / max row sums
     rs = d.sum(1)
     assert rs.min() - 1e-9 <= lam_ref[-1] <= rs.max() + 1e-9
+
+
+def _col_slice(S, c0, c1):
+    """Columns [c0, c1) of a CSR (global column indices kept) — the oracle's view of a panel."""
+    keep = (S.col >= c0) & (S.col < c1)
+    rows = np.repeat(np.arange(S.m), np.diff(S.row_ptr))
+    rp = np.zeros(S.m + 1, np.int64)
+    np.add.at(rp, rows[keep] + 1, 1)
+    return synth.CSR(S.m, S.n, np.cumsum(rp), S.col[keep], S.val[keep])
+
+
+def _panel_pi_worker(rank, world, port, steps, P, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 1024 * world
+        A = synth.uniform(n, n, 30, 52, val_mode=1)
+        m_loc = n // world
+        S = cbd.slice_rows(A, rank * m_loc, (rank + 1) * m_loc)
+        h = cb.build(S, device=-1, col_panels=P)  # the real builder's panel cuts
+        panels = [cb.panel_bounds(h, p) for p in range(h.info["n_panels"])]
+        subs = [_col_slice(S, c0, c1) for c0, c1 in panels]
+        ran = []
+
+        def spmv_panel(p, x, ss, y, zero):  # oracle stand-in for cbspmv_spmv_panel
+            ran.append(p)
+            c0, c1 = panels[p]
+            xs = np.zeros(S.n)
+            xs[c0:c1] = x.numpy()[c0:c1] / np.sqrt(ss.item())
+            part = torch.from_numpy(oracle.spmv_csr(subs[p], xs)[0])
+            if zero:
+                y.copy_(part)
+            else:
+                y.add_(part)
+
+        def sumsq(y, out):
+            out.fill_(float(torch.dot(y, y)))
+
+        it = cbd.PanelPowerIteration(
+            spmv_panel, sumsq,
+            all_reduce_sum_async=lambda t: dist.all_reduce(t, async_op=True),
+            broadcast_async=lambda t, src: dist.broadcast(t, src=src, async_op=True),
+            panels=panels, row_bounds=[(r * m_loc, (r + 1) * m_loc) for r in range(world)], rank=rank)
+        xa = torch.ones(n, dtype=torch.float64)
+        xb = torch.full((n,), float("nan"), dtype=torch.float64)
+        ss = torch.tensor([float(n)], dtype=torch.float64)
+        x, ss = it.run(xa, xb, ss, steps)
+        own_first = all(it.owners[p] == [rank] for p in it.order[:sum(ow == [rank] for ow in it.owners)])
+        q.put((rank, float(ss.item()), x.numpy().copy(), ran[:len(panels)], it.order, own_first))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,P", [(2, 2), (2, 5), (3, 5)])
+def test_panel_power_iteration_overlap_matches_recurrence(world, P):
+    """NEXT-1 (i) host logic: per-owner broadcasts + panels in arrival order == the plain recurrence."""
+    steps = 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_panel_pi_worker, args=(r, world, port, steps, P, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 1024 * world
+    d = synth.uniform(n, n, 30, 52, val_mode=1).to_dense()
+    x = np.ones(n)
+    ss = float(n)
+    for _ in range(steps):
+        y = d @ (x / np.sqrt(ss))
+        ss = float(y @ y)
+        x = y
+    for rank, ss_r, x_r, ran, order, own_first in res:
+        assert np.isclose(ss_r, ss, rtol=1e-12)
+        assert np.allclose(x_r, x, rtol=1e-11)  # every rank ends with the complete iterate
+        assert ran == order and own_first

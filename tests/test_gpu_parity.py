@@ -430,3 +430,44 @@ def test_mixed_host_scaled_and_panels(P):
     cb.spmv_scaled(h, xd, ss, ys)
     torch.cuda.synchronize()
     check_rows(ys.cpu().numpy() * 2.0, y_ref, R, 1e-12)
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_power_iteration_overlapped_panels_device(P):
+    """NEXT-1 (i) driver on the device (N=1: panels in order, no broadcasts) == the recurrence;
+    the all-ones matrix keeps lambda = 50 exactly through cbspmv_spmv_panel as well."""
+    _ok()
+    from paper_2605_18515_b200 import dist as cbd
+    A = synth.uniform(1 << 13, 1 << 13, 50, 51, val_mode=1)
+    h = cb.build(A, device=0, col_panels=P)
+    assert h.info["n_panels"] == P
+    x, ss = cbd.power_iteration_overlapped(h, torch.ones(A.n, dtype=torch.float64, device=DEV), 20)
+    d = A.to_dense()
+    xr, ssr = np.ones(A.n), float(A.n)
+    for _ in range(20):
+        yr = d @ (xr / np.sqrt(ssr))
+        ssr = float(yr @ yr)
+        xr = yr
+    assert np.isclose(float(ss.item()), ssr, rtol=1e-12)
+    assert np.allclose(x.cpu().numpy(), xr, rtol=1e-11, atol=0)
+    B = synth.uniform(1 << 12, 1 << 12, 50, 51, val_mode=3)
+    hb = cb.build(B, device=0, col_panels=P)
+    lams = []
+    cbd.power_iteration_overlapped(hb, torch.ones(B.n, dtype=torch.float64, device=DEV), 6,
+                                   on_step=lambda k, x, s: lams.append(float(s.item()) ** 0.5))
+    assert lams == [50.0] * 6
+
+
+def test_spmv_panel_sum_equals_spmv():
+    _ok()
+    A = synth.make("rmat", small=True)
+    x = synth.vector(A.n, synth.VEC_INT7)
+    h = cb.build(A, device=0, col_panels=4)
+    xd = torch.from_numpy(x).to(DEV)
+    y = torch.full((A.m,), float("nan"), dtype=torch.float64, device=DEV)
+    for k in range(4):
+        cb.spmv_panel(h, k, xd, None, y, k == 0)
+    torch.cuda.synchronize()
+    y_ref, _ = oracle.spmv_csr(A, x)
+    assert np.array_equal(y.cpu().numpy(), y_ref)  # exact-integer data: bitwise
+    assert [cb.panel_bounds(h, k)[0] for k in range(4)][0] == 0 and cb.panel_bounds(h, 3)[1] == A.n
