@@ -504,30 +504,33 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
     for (int64_t b = 0; b < nb; b++) order[cnt[maxk - nnzb[b]]++] = b;
     // min-heap over (loads, tb_id) as a bucket queue: loads <= W*B*B, and the minimum load
     // never decreases (each pop re-pushes with a larger load), so a forward cursor suffices.
+    // A bucket is only pushed to while the cursor is below it (pushes go to load + nnz > cur)
+    // and only popped once the cursor has reached it, so each bucket is a plain vector sorted
+    // once by tb_id when the cursor arrives (usually already sorted) and then read in order:
+    // the pop order is exactly the heap's (load, tb_id) order.
     const int64_t maxload = (int64_t)W * maxk;
     std::vector<std::vector<uint32_t>> bucket((size_t)maxload + 1);
     bucket[0].resize((size_t)TB);
-    for (int64_t t = 0; t < TB; t++) bucket[0][t] = (uint32_t)t;  // ascending = a valid min-heap
+    for (int64_t t = 0; t < TB; t++) bucket[0][t] = (uint32_t)t;
     std::vector<int32_t> warps(TB, 0);
     std::vector<uint32_t> slot_tb(nb);
     std::vector<int32_t> slot_w(nb);
     int64_t cur = 0;
-    auto gt = std::greater<uint32_t>();
+    size_t pos = 0;
     for (int64_t i = 0; i < nb; i++) {
-      while (bucket[cur].empty()) cur++;
-      std::vector<uint32_t> &bk = bucket[cur];
-      std::pop_heap(bk.begin(), bk.end(), gt);
-      uint32_t tb = bk.back();
-      bk.pop_back();
+      while (pos == bucket[cur].size()) {
+        std::vector<uint32_t>().swap(bucket[cur]);
+        cur++;
+        pos = 0;
+        std::vector<uint32_t> &v = bucket[cur];
+        if (!std::is_sorted(v.begin(), v.end())) std::sort(v.begin(), v.end());
+      }
+      const uint32_t tb = bucket[cur][pos++];
       int64_t b = order[i];
       slot_tb[b] = tb; slot_w[b] = warps[tb];        // end <- tb_id*8 + warps
       c.tb_load[tb] += nnzb[b];                      // loads <- loads + nnz
       warps[tb]++;                                   // warps <- warps + 1
-      if (warps[tb] < W) {                           // if warps < 8: push
-        std::vector<uint32_t> &nbk = bucket[(size_t)c.tb_load[tb]];
-        nbk.push_back(tb);
-        std::push_heap(nbk.begin(), nbk.end(), gt);
-      }
+      if (warps[tb] < W) bucket[(size_t)c.tb_load[tb]].push_back(tb);  // if warps < 8: push
     }
     // "parallel sort(blk_idx_array, cmp_end)": ends are unique, so position = tb_ptr[tb] + w.
     for (int64_t t = 0; t < TB; t++) c.tb_ptr[t + 1] = c.tb_ptr[t] + warps[t];

@@ -460,7 +460,7 @@ def test_power_iteration_overlapped_panels_device(P):
 
 def test_spmv_panel_sum_equals_spmv():
     _ok()
-    A = synth.make("rmat", small=True)
+    A = synth.random_csr(3000, 2600, 0.01, 17, val_mode=2, pattern="hub")  # exact-integer values
     x = synth.vector(A.n, synth.VEC_INT7)
     h = cb.build(A, device=0, col_panels=4)
     xd = torch.from_numpy(x).to(DEV)
