@@ -28,7 +28,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcbspmv.so")
+LIB_PATH = os.environ.get("CBSPMV_LIB") or os.path.join(_HERE, "libcbspmv.so")  # override: A/B of builds
 _lib = None
 
 F64, F32, F32F64 = 0, 1, 2  # F32F64: fp32 matrix values, fp64 x / y / accumulation (R-24)

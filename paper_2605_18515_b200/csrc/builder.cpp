@@ -655,6 +655,7 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     if (!p) { *err = "host allocation of the page stream failed"; return CBSPMV_ENOMEM; }
     s->bytes = (uint8_t *)p;
   }
+  tm.lap(s->pinned ? "stream: pinned alloc" : "stream: pageable alloc");
   parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
     std::vector<uint32_t> w;
     std::vector<uint16_t> items;

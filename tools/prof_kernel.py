@@ -16,7 +16,7 @@ ap.add_argument("--launches", type=int, default=3)
 ap.add_argument("--small", action="store_true")
 a = ap.parse_args()
 A = synth.make(a.config, small=a.small)
-tdt = torch.float64 if a.dtype == "f64" else torch.float32
+tdt = torch.float32 if a.dtype == "f32" else torch.float64
 h = cb.build(A, dtype=a.dtype, device=0, keep_host=0)
 x = torch.from_numpy(synth.vector(A.n, 0, 7)).to("cuda:0", tdt)
 y = torch.empty(A.m, dtype=tdt, device="cuda:0")
