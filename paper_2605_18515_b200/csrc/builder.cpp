@@ -409,6 +409,81 @@ int block_stats(const Csr &A, const cbspmv_options_t &o, int64_t *nb_pre, int64_
   return CBSPMV_OK;
 }
 
+// a7 TB-Load-Balance (Alg. 2) on the natural-order block arrays, then the permutation of the five
+// high-level arrays into slot order (c.nb, c.blk, c.W set; mtx untouched: VPs travel with blocks).
+void balance_and_permute(Canon &c, const cbspmv_options_t &o, const int32_t *nbr, const int32_t *nbc,
+                         const int32_t *nnzb, const uint8_t *ntype, const uint64_t *nvp, PhaseTimer &tm) {
+  const int64_t nb = c.nb;
+  const int B = c.blk, W = c.W, T = resolve_threads(o.host_threads);
+  const int64_t TB = (nb + W - 1) / W;
+  c.T = TB;
+  c.tb_ptr.assign((size_t)TB + 1, 0);
+  c.tb_load.assign((size_t)TB, 0);
+  c.tb_load_nat.assign((size_t)TB, 0);
+  for (int64_t b = 0; b < nb; b++) c.tb_load_nat[b / W] += nnzb[b];
+  std::vector<int64_t> perm(nb);  // slot-order position -> natural block index
+  if (o.balance && nb > 0) {
+    // "parallel sort(blk_idx_array, cmp_nnz)": nnz descending, ties by index ascending (R-12);
+    // a stable counting sort over nnz in [1, B*B].
+    const int maxk = B * B;
+    std::vector<int64_t> cnt(maxk + 2, 0);
+    for (int64_t b = 0; b < nb; b++) cnt[maxk - nnzb[b]]++;
+    int64_t acc = 0;
+    for (int k = 0; k <= maxk; k++) { int64_t t = cnt[k]; cnt[k] = acc; acc += t; }
+    std::vector<int64_t> order(nb);
+    for (int64_t b = 0; b < nb; b++) order[cnt[maxk - nnzb[b]]++] = b;
+    // min-heap over (loads, tb_id) as a bucket queue: loads <= W*B*B, and the minimum load
+    // never decreases (each pop re-pushes with a larger load), so a forward cursor suffices.
+    // A bucket is only pushed to while the cursor is below it (pushes go to load + nnz > cur)
+    // and only popped once the cursor has reached it, so each bucket is a plain vector sorted
+    // once by tb_id when the cursor arrives (usually already sorted) and then read in order:
+    // the pop order is exactly the heap's (load, tb_id) order.
+    const int64_t maxload = (int64_t)W * maxk;
+    std::vector<std::vector<uint32_t>> bucket((size_t)maxload + 1);
+    bucket[0].resize((size_t)TB);
+    for (int64_t t = 0; t < TB; t++) bucket[0][t] = (uint32_t)t;
+    std::vector<int32_t> warps(TB, 0);
+    std::vector<uint32_t> slot_tb(nb);
+    std::vector<int32_t> slot_w(nb);
+    int64_t cur = 0;
+    size_t pos = 0;
+    for (int64_t i = 0; i < nb; i++) {
+      while (pos == bucket[cur].size()) {
+        std::vector<uint32_t>().swap(bucket[cur]);
+        cur++;
+        pos = 0;
+        std::vector<uint32_t> &v = bucket[cur];
+        if (!std::is_sorted(v.begin(), v.end())) std::sort(v.begin(), v.end());
+      }
+      const uint32_t tb = bucket[cur][pos++];
+      int64_t b = order[i];
+      slot_tb[b] = tb; slot_w[b] = warps[tb];        // end <- tb_id*8 + warps
+      c.tb_load[tb] += nnzb[b];                      // loads <- loads + nnz
+      warps[tb]++;                                   // warps <- warps + 1
+      if (warps[tb] < W) bucket[(size_t)c.tb_load[tb]].push_back(tb);  // if warps < 8: push
+    }
+    // "parallel sort(blk_idx_array, cmp_end)": ends are unique, so position = tb_ptr[tb] + w.
+    for (int64_t t = 0; t < TB; t++) c.tb_ptr[t + 1] = c.tb_ptr[t] + warps[t];
+    for (int64_t b = 0; b < nb; b++) perm[c.tb_ptr[slot_tb[b]] + slot_w[b]] = b;
+  } else {
+    for (int64_t b = 0; b < nb; b++) perm[b] = b;
+    for (int64_t t = 0; t < TB; t++) {
+      c.tb_ptr[t + 1] = std::min<int64_t>(nb, (t + 1) * W);
+      c.tb_load[t] = c.tb_load_nat[t];
+    }
+  }
+  tm.lap("a7 Alg. 2 greedy");
+  // permute the five high-level arrays (vp_per_blk[i] <- vp_per_blk_old[ori])
+  c.br.resize(nb); c.bc.resize(nb); c.nnzb.resize(nb); c.type.resize(nb); c.vp.resize(nb);
+  parallel_for(nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t i = lo; i < hi; i++) {
+      int64_t b = perm[i];
+      c.br[i] = nbr[b]; c.bc[i] = nbc[b]; c.nnzb[i] = nnzb[b]; c.type[i] = ntype[b]; c.vp[i] = nvp[b];
+    }
+  });
+  tm.lap("a7 permute");
+}
+
 int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::string *err) {
   const int B = o.blk, W = o.warps_per_tb, threads = o.host_threads;
   const int64_t S = A.val_size;
@@ -484,74 +559,7 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
   for (int64_t b = 0; b < nb; b++) c.fmt_count[ntype[b]]++;
 
   tm.lap("a6 fill pass");
-  // a7. TB-Load-Balance (Alg. 2).
-  const int64_t TB = (nb + W - 1) / W;
-  c.T = TB;
-  c.tb_ptr.assign((size_t)TB + 1, 0);
-  c.tb_load.assign((size_t)TB, 0);
-  c.tb_load_nat.assign((size_t)TB, 0);
-  for (int64_t b = 0; b < nb; b++) c.tb_load_nat[b / W] += nnzb[b];
-  std::vector<int64_t> perm(nb);  // slot-order position -> natural block index
-  if (o.balance && nb > 0) {
-    // "parallel sort(blk_idx_array, cmp_nnz)": nnz descending, ties by index ascending (R-12);
-    // a stable counting sort over nnz in [1, B*B].
-    const int maxk = B * B;
-    std::vector<int64_t> cnt(maxk + 2, 0);
-    for (int64_t b = 0; b < nb; b++) cnt[maxk - nnzb[b]]++;
-    int64_t acc = 0;
-    for (int k = 0; k <= maxk; k++) { int64_t t = cnt[k]; cnt[k] = acc; acc += t; }
-    std::vector<int64_t> order(nb);
-    for (int64_t b = 0; b < nb; b++) order[cnt[maxk - nnzb[b]]++] = b;
-    // min-heap over (loads, tb_id) as a bucket queue: loads <= W*B*B, and the minimum load
-    // never decreases (each pop re-pushes with a larger load), so a forward cursor suffices.
-    // A bucket is only pushed to while the cursor is below it (pushes go to load + nnz > cur)
-    // and only popped once the cursor has reached it, so each bucket is a plain vector sorted
-    // once by tb_id when the cursor arrives (usually already sorted) and then read in order:
-    // the pop order is exactly the heap's (load, tb_id) order.
-    const int64_t maxload = (int64_t)W * maxk;
-    std::vector<std::vector<uint32_t>> bucket((size_t)maxload + 1);
-    bucket[0].resize((size_t)TB);
-    for (int64_t t = 0; t < TB; t++) bucket[0][t] = (uint32_t)t;
-    std::vector<int32_t> warps(TB, 0);
-    std::vector<uint32_t> slot_tb(nb);
-    std::vector<int32_t> slot_w(nb);
-    int64_t cur = 0;
-    size_t pos = 0;
-    for (int64_t i = 0; i < nb; i++) {
-      while (pos == bucket[cur].size()) {
-        std::vector<uint32_t>().swap(bucket[cur]);
-        cur++;
-        pos = 0;
-        std::vector<uint32_t> &v = bucket[cur];
-        if (!std::is_sorted(v.begin(), v.end())) std::sort(v.begin(), v.end());
-      }
-      const uint32_t tb = bucket[cur][pos++];
-      int64_t b = order[i];
-      slot_tb[b] = tb; slot_w[b] = warps[tb];        // end <- tb_id*8 + warps
-      c.tb_load[tb] += nnzb[b];                      // loads <- loads + nnz
-      warps[tb]++;                                   // warps <- warps + 1
-      if (warps[tb] < W) bucket[(size_t)c.tb_load[tb]].push_back(tb);  // if warps < 8: push
-    }
-    // "parallel sort(blk_idx_array, cmp_end)": ends are unique, so position = tb_ptr[tb] + w.
-    for (int64_t t = 0; t < TB; t++) c.tb_ptr[t + 1] = c.tb_ptr[t] + warps[t];
-    for (int64_t b = 0; b < nb; b++) perm[c.tb_ptr[slot_tb[b]] + slot_w[b]] = b;
-  } else {
-    for (int64_t b = 0; b < nb; b++) perm[b] = b;
-    for (int64_t t = 0; t < TB; t++) {
-      c.tb_ptr[t + 1] = std::min<int64_t>(nb, (t + 1) * W);
-      c.tb_load[t] = c.tb_load_nat[t];
-    }
-  }
-  tm.lap("a7 Alg. 2 greedy");
-  // permute the five high-level arrays (vp_per_blk[i] <- vp_per_blk_old[ori])
-  c.br.resize(nb); c.bc.resize(nb); c.nnzb.resize(nb); c.type.resize(nb); c.vp.resize(nb);
-  parallel_for(nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
-    for (int64_t i = lo; i < hi; i++) {
-      int64_t b = perm[i];
-      c.br[i] = nbr[b]; c.bc[i] = nbc[b]; c.nnzb[i] = nnzb[b]; c.type[i] = ntype[b]; c.vp[i] = nvp[b];
-    }
-  });
-  tm.lap("a7 permute");
+  balance_and_permute(c, o, nbr.data(), nbc.data(), nnzb.data(), ntype.data(), nvp.data(), tm);
   return CBSPMV_OK;
 }
 
@@ -650,8 +658,16 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
   s->page_off = off;
   if (total > 0) {
     void *p = nullptr;
-    if (cudaHostAlloc(&p, (size_t)total, cudaHostAllocDefault) == cudaSuccess) s->pinned = true;
-    else { cudaGetLastError(); p = std::malloc((size_t)total); s->pinned = false; }
+    // Pageable by default: pinning a multi-GB buffer costs more (measured 2.7 s for the 4.2 GB
+    // clustered stream on the B200 host) than the slower pageable copy saves.
+    static const bool want_pinned = std::getenv("CBSPMV_PINNED_STREAM") != nullptr;
+    if (want_pinned && cudaHostAlloc(&p, (size_t)total, cudaHostAllocDefault) == cudaSuccess) {
+      s->pinned = true;
+    } else {
+      if (want_pinned) cudaGetLastError();
+      p = std::malloc((size_t)total);
+      s->pinned = false;
+    }
     if (!p) { *err = "host allocation of the page stream failed"; return CBSPMV_ENOMEM; }
     s->bytes = (uint8_t *)p;
   }

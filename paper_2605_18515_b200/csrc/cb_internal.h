@@ -106,7 +106,7 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
 
 // Device page stream built from the canonical format.
 struct Stream {
-  uint8_t *bytes = nullptr;        // pinned host staging (cudaHostAlloc) or malloc
+  uint8_t *bytes = nullptr;        // host staging: malloc (default) or cudaHostAlloc (CBSPMV_PINNED_STREAM)
   bool pinned = false;
   int64_t nbytes = 0;
   std::vector<uint64_t> page_off;  // n_pages + 1

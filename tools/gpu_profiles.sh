@@ -9,3 +9,4 @@ for c in ${CONFIGS:-clustered rmat}; do
 done
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo bench_rc=$?
 tail -1 gpurun_out/bench_default.log
+CBSPMV_BUILD_TIMING=1 timeout 900 python tools/build_timing.py clustered rmat uniform > gpurun_out/build_timing.log 2>&1; echo timing_rc=$?
