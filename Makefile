@@ -39,10 +39,13 @@ $(CSRC)/%.o: $(CSRC)/%.cpp $(CSRC)/cb_internal.h include/cbspmv.h
 $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/cb_internal.h include/cbspmv.h
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
 
-$(LIB): $(HOST_OBJS) $(CSRC)/kernels.o
+$(CSRC)/gpu_builder.o: $(CSRC)/gpu_builder.cu $(CSRC)/cb_internal.h include/cbspmv.h
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(CSRC)/ptxas_builder.log || (cat $(CSRC)/ptxas_builder.log; false)
+
+$(LIB): $(HOST_OBJS) $(CSRC)/kernels.o $(CSRC)/gpu_builder.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lpthread
 
 clean:
-	rm -f synth/libsynth.so oracle/liboracle.so $(LIB) $(CSRC)/*.o $(CSRC)/ptxas.log
+	rm -f synth/libsynth.so oracle/liboracle.so $(LIB) $(CSRC)/*.o $(CSRC)/ptxas*.log
 
 .PHONY: all synth oracle lib clean

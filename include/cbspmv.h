@@ -76,6 +76,10 @@ typedef struct {
                              (all rows, columns [c_k, c_k+1), 16-aligned) runs the whole pipeline as
                              its own matrix; cbspmv_spmv zeroes y once and runs the panels in order so
                              each panel's slice of x stays L2-resident. */
+  int32_t device_build;   /* 1 = steps a2..a6 on the GPU (radix sorts, scans, one warp per record;
+                             SURVEY §8(f) NEXT-3), a1 and Alg. 2 on the host; the canonical format is
+                             byte-identical to the host build.  Needs device >= 0 and < 2^31 stored
+                             entries per panel.  0 = host build (default). */
 } cbspmv_options_t;
 
 typedef struct {

@@ -41,7 +41,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSORTED", 3: "ENOMEM", 4: "ECUDA", 5: "EDI
 class Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32)] + [(k, ctypes.c_int32) for k in (
         "blk", "th0_num", "th0_den", "ss_limit", "th1", "th2", "warps_per_tb", "agg_mode", "balance",
-        "force_format", "device", "host_threads", "keep_host", "col_panels")]
+        "force_format", "device", "host_threads", "keep_host", "col_panels", "device_build")]
 
 
 class Info(ctypes.Structure):

@@ -29,20 +29,6 @@
 
 namespace cb {
 
-namespace {
-// Phase timing of the host pipeline (env CBSPMV_BUILD_TIMING=1 prints to stderr).
-struct PhaseTimer {
-  bool on = std::getenv("CBSPMV_BUILD_TIMING") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void lap(const char *what) {
-    if (!on) return;
-    auto n = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[cbspmv build] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
-    t = n;
-  }
-};
-}  // namespace
-
 int resolve_threads(int t) {
   if (t > 0) return t;
   unsigned h = std::thread::hardware_concurrency();
@@ -596,7 +582,8 @@ void free_stream(Stream *s) {
   s->bytes = nullptr; s->nbytes = 0; s->page_off.clear();
 }
 
-int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, std::string *err) {
+int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
+                 std::string *err) {
   const int T = resolve_threads(threads);
   PhaseTimer tm;
   std::vector<int64_t> rec(c.nb);
@@ -656,7 +643,18 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
   tm.lap("stream: page plan");
   s->nbytes = total;
   s->page_off = off;
-  if (total > 0) {
+  if (plan) {  // device fill: page prefixes (header | descriptors | items) in a compact buffer
+    plan->meta_off.assign((size_t)npages + 1, 0);
+    for (int64_t p = 0; p < npages; p++) {
+      const int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
+      plan->meta_off[p + 1] = plan->meta_off[p] + (uint64_t)(kPageHeader + kDescBytes * (b1 - b0) +
+                                                             round_up(4 * count_items(b0, b1), 16));
+    }
+    plan->meta.assign((size_t)plan->meta_off[npages], 0);
+    plan->rec_dst.assign((size_t)c.nb, 0);
+    plan->res_dst.assign(c.agg ? (size_t)c.nb : 0, 0);
+    plan->ncol = ncol;
+  } else if (total > 0) {
     void *p = nullptr;
     // Pageable by default: pinning a multi-GB buffer costs more (measured 2.7 s for the 4.2 GB
     // clustered stream on the B200 host) than the slower pageable copy saves.
@@ -671,17 +669,17 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     if (!p) { *err = "host allocation of the page stream failed"; return CBSPMV_ENOMEM; }
     s->bytes = (uint8_t *)p;
   }
-  tm.lap(s->pinned ? "stream: pinned alloc" : "stream: pageable alloc");
+  tm.lap(plan ? "stream: device plan alloc" : s->pinned ? "stream: pinned alloc" : "stream: pageable alloc");
   parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
     std::vector<uint32_t> w;
     std::vector<uint16_t> items;
     std::vector<uint32_t> iwords;
     for (int64_t p = lo; p < hi; p++) {
-      uint8_t *page = s->bytes + off[p];
+      uint8_t *page = plan ? plan->meta.data() + plan->meta_off[p] : s->bytes + off[p];
       const int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
       const int64_t nblk = b1 - b0;
       w.assign((size_t)nblk, 0);
-      std::memset(page, 0, (size_t)(off[p + 1] - off[p]));
+      if (!plan) std::memset(page, 0, (size_t)(off[p + 1] - off[p]));
       // work items
       items.clear();
       iwords.clear();
@@ -736,6 +734,12 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
         d.w = pack_w((uint32_t)k, (uint32_t)type, (uint32_t)ncol[i], is_head, is_head ? gsize[i - b0] : 1u, 0u) |
               w[i - b0];
         std::memcpy(page + kPageHeader + kDescBytes * (i - b0), &d, sizeof(d));
+        if (plan) {  // records and restore entries are copied on the device (fill_stream_device)
+          plan->rec_dst[i] = off[p] + (uint64_t)body;
+          if (c.agg) plan->res_dst[i] = off[p] + (uint64_t)pos;
+          pos += rec[i];
+          continue;
+        }
         if (c.agg) {
           const uint32_t *seg = c.restore.data() + c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk;
           std::memcpy(page + pos, seg, (size_t)ncol[i] * 4);

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <string>
 
@@ -57,6 +58,7 @@ struct Part {
   uint64_t *d_page_off = nullptr;
   uint32_t *d_cta_page = nullptr;
   int64_t stream_bytes = 0, n_pages = 0;
+  std::unique_ptr<cb::DevCanon> dc;  // device builder: records still on the device until the stream fill
 };
 
 // Rows x columns [c0, c1) of a canonical CSR (columns keep their global index).
@@ -105,6 +107,7 @@ cbspmv_status_t cbspmv_default_options(cbspmv_options_t *o) {
   o->host_threads = 0;
   o->keep_host = 1;
   o->col_panels = 0;
+  o->device_build = 0;
   return CBSPMV_OK;
 }
 
@@ -130,7 +133,9 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   const char *env = std::getenv("CBSPMV_PAGE_BYTES");
   int cap = env ? std::atoi(env) : cb::kDefaultStageCap;
   cap = (int)cb::round_up(std::max(cap, 1024), 16);
-  int st = cb::build_stream(c, cap, vec_bytes(dtype), o.host_threads, &S, err);
+  cb::StreamPlan plan;
+  const bool on_device = P->dc != nullptr;  // records on the device: fill the stream there
+  int st = cb::build_stream(c, cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   const int64_t npages = (int64_t)S.page_off.size() - 1;
   CbDevice &D = P->dev;
@@ -147,6 +152,7 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   }
   cta[D.grid] = (uint32_t)npages;
   const double t1 = now();
+  cb::PhaseTimer tm;
   cudaError_t e = cudaSuccess;
   if (S.nbytes > 0) e = cudaMalloc(&P->d_stream, (size_t)S.nbytes);
   if (e == cudaSuccess) e = cudaMalloc(&P->d_page_off, S.page_off.size() * sizeof(uint64_t));
@@ -157,14 +163,24 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
     *err = std::string("device allocation: ") + cudaGetErrorString(e);
     return CBSPMV_ENOMEM;
   }
-  // "transferred to the GPU in a single operation"
-  if (S.nbytes > 0) e = cudaMemcpyAsync(P->d_stream, S.bytes, (size_t)S.nbytes, cudaMemcpyHostToDevice, cs);
+  // "transferred to the GPU in a single operation"; device builder: filled in place
+  tm.lap("upload: device allocations");
+  if (on_device) {
+    st = cb::fill_stream_device(c, *P->dc, S, plan, cs, P->d_stream, err);
+    tm.lap("upload: device stream fill");
+    P->dc.reset();
+    tm.lap("upload: free device records");
+    if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
+  } else if (S.nbytes > 0) {
+    e = cudaMemcpyAsync(P->d_stream, S.bytes, (size_t)S.nbytes, cudaMemcpyHostToDevice, cs);
+  }
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(P->d_page_off, S.page_off.data(), S.page_off.size() * sizeof(uint64_t),
                         cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(P->d_cta_page, cta.data(), cta.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  tm.lap("upload: copies + sync");
   cb::free_stream(&S);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -181,7 +197,14 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
 // Build + upload one panel's format (the Fig. 7 pipeline on A[:, c0:c1)).
 static int build_part(const cb::Csr &A, const cbspmv_options_t &o, int dtype, cudaStream_t cs, Part *P,
                       double *t_up, std::string *err) {
-  int st = cb::build_canonical(A, o, &P->canon, err);
+  int st;
+  if (o.device >= 0 && o.device_build) {
+    P->dc.reset(new cb::DevCanon());
+    st = cb::build_canonical_device(A, o, cs, &P->canon, P->dc.get(), o.keep_host != 0, err);
+    if (st != CBSPMV_OK) P->dc.reset();
+  } else {
+    st = cb::build_canonical(A, o, &P->canon, err);
+  }
   if (st != CBSPMV_OK || o.device < 0) return st;
   return upload_part(o, dtype, cs, P, t_up, err);
 }

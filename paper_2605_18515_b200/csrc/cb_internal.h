@@ -1,7 +1,9 @@
 // cb_internal.h — shared internals of libcbspmv (host builder, C ABI, kernels).
 // Product path only; nothing here is shared with oracle/.
 #pragma once
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <functional>
 #include <memory>
@@ -111,8 +113,32 @@ struct Stream {
   int64_t nbytes = 0;
   std::vector<uint64_t> page_off;  // n_pages + 1
 };
-// x_size: bytes of one x element (sizes the non-aggregated x tiles that follow each page)
-int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, std::string *err);
+// Device-fill plan of the page stream (device builder): the page prefixes (header | descriptors |
+// items) in a compact buffer, and per slot-order block the stream offsets of its record and restore
+// entries; the records themselves are copied on the device (fill_stream_device).
+struct StreamPlan {
+  std::vector<uint8_t> meta;
+  std::vector<uint64_t> meta_off;          // n_pages + 1
+  std::vector<uint64_t> rec_dst, res_dst;  // per block (res_dst only when aggregated)
+  std::vector<int32_t> ncol;               // x-tile columns per block
+};
+// x_size: bytes of one x element (sizes the non-aggregated x tiles that follow each page).
+// plan == nullptr: the whole stream is written to host memory (s->bytes); otherwise only the plan.
+int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
+                 std::string *err);
+
+// Device-resident canonical arrays kept by the device builder for fill_stream_device.
+struct DevCanon {
+  uint8_t *mtx = nullptr;
+  uint32_t *restore = nullptr;
+  uint64_t *cols_offset = nullptr;
+  void release();
+  ~DevCanon() { release(); }
+};
+// Write the device page stream (d_stream, s.nbytes) from the plan and the device-resident records
+// (gpu_builder.cu): page prefixes, restore entries, records (DENSE in the lane-major layout).
+int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, const StreamPlan &plan, void *stream,
+                       uint8_t *d_stream, std::string *err);
 void free_stream(Stream *s);
 
 // Matrix Market coordinate files (mmio.cpp)
@@ -129,6 +155,29 @@ struct CbsmExt {
 int write_cbsm(FILE *f, const Canon &c, const CbsmExt &x, std::string *err);
 int read_cbsm(FILE *f, Canon *out, CbsmExt *x, std::string *err);  // validates (validate_canon)
 int validate_canon(const Canon &c, const CbsmExt &x, std::string *err);
+
+// Phase timing of the builders (env CBSPMV_BUILD_TIMING=1 prints to stderr).
+struct PhaseTimer {
+  bool on = std::getenv("CBSPMV_BUILD_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char *what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cbspmv build] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+
+// a7 + permute on natural-order block arrays (builder.cpp; shared by the host and device builders)
+void balance_and_permute(Canon &c, const cbspmv_options_t &o, const int32_t *nbr, const int32_t *nbc,
+                         const int32_t *nnzb, const uint8_t *ntype, const uint64_t *nvp, PhaseTimer &tm);
+
+// Steps a2..a6 on the GPU (gpu_builder.cu, NEXT-3): the same canonical format as build_canonical,
+// byte for byte; a1 runs on the host first, a7 on the host after.
+// dc != nullptr: the records, restore_cols and cols_offset stay on the device in *dc (for
+// fill_stream_device) and are downloaded into *out only when download_records is set.
+int build_canonical_device(const Csr &A, const cbspmv_options_t &o, void *stream, Canon *out, DevCanon *dc,
+                           bool download_records, std::string *err);
 
 // Threads
 void parallel_for(int64_t n, int threads, int64_t grain, const std::function<void(int64_t, int64_t, int)> &fn);

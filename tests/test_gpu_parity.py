@@ -220,11 +220,13 @@ def decode_stream(stream, page_off):
 
 @pytest.mark.parametrize("name", ["laplace", "rmat", "clustered"])
 @pytest.mark.parametrize("dtype", ["f64", "f32f64"])
-def test_device_stream_encodes_canonical_format(name, dtype):
-    """What is on the device is exactly the canonical format (slot order), records byte-equal."""
+@pytest.mark.parametrize("device_build", [0, 1])
+def test_device_stream_encodes_canonical_format(name, dtype, device_build):
+    """What is on the device is exactly the canonical format (slot order), records byte-equal;
+    device_build=1: the stream is filled on the device from the device-built records."""
     _ok()
     A = synth.make(name, small=True)
-    h = cb.build(A, dtype=dtype, device=0)
+    h = cb.build(A, dtype=dtype, device=0, device_build=device_build)
     ex = cb.export(h)
     s, po = cb.download_stream(h)
     blocks = decode_stream(s, po)

@@ -13,7 +13,7 @@ for name in (sys.argv[1:] or ["clustered", "rmat"]):
     A = synth.make(name)
     gen = time.perf_counter() - t
     t = time.perf_counter()
-    h = cb.build(A, device=0, keep_host=0)
+    h = cb.build(A, device=0, keep_host=0, device_build=int(os.environ.get("DEVICE_BUILD", "0")))
     wall = time.perf_counter() - t
     i = h.info
     print(f"{name}: gen {gen:.2f} s, build wall {wall:.2f} s (build_seconds {i['build_seconds']:.2f}, "
