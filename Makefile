@@ -42,7 +42,10 @@ $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/cb_internal.h include/cbspmv.h
 $(CSRC)/gpu_builder.o: $(CSRC)/gpu_builder.cu $(CSRC)/cb_internal.h include/cbspmv.h
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(CSRC)/ptxas_builder.log || (cat $(CSRC)/ptxas_builder.log; false)
 
-$(LIB): $(HOST_OBJS) $(CSRC)/kernels.o $(CSRC)/gpu_builder.o
+$(CSRC)/exchange.o: $(CSRC)/exchange.cu $(CSRC)/cb_internal.h include/cbspmv.h
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(CSRC)/ptxas_exchange.log || (cat $(CSRC)/ptxas_exchange.log; false)
+
+$(LIB): $(HOST_OBJS) $(CSRC)/kernels.o $(CSRC)/gpu_builder.o $(CSRC)/exchange.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lpthread
 
 clean:

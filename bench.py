@@ -384,7 +384,15 @@ def run_power(args, rank, world, local_rank):
     info = h.info
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     x0 = torch.ones(A.n, dtype=tdt, device=dev)
-    if args.no_overlap:
+    fused = None
+    if args.exchange == "fused":
+        # NEXT-1 (ii): y shards pushed into every peer's next iterate by one kernel over peer
+        # memory (CUDA IPC mappings), the next step gated by device flags
+        fused = dist.FusedPowerIteration(h, A.n, "f32" if args.dtype == "f32" else "f64", world, rank, local_rank)
+
+        def run_steps(n):
+            return fused.run(x0, n)
+    elif args.exchange == "nccl" or args.no_overlap:
         def run_steps(n):
             return dist.power_iteration_device(h, x0, n, world)
     else:
@@ -412,6 +420,8 @@ def run_power(args, rank, world, local_rank):
     torch.cuda.synchronize()
     kernel_ms = k0.elapsed_time(k1) / args.steps
     lam = float(ss.item()) ** 0.5
+    if fused is not None and fused.timed_out():
+        raise RuntimeError("fused exchange: a device wait timed out (a peer never published)")
     peak, peak_src = peaks()
     if rank == 0:
         line = {
@@ -422,17 +432,26 @@ def run_power(args, rank, world, local_rank):
                        "name": "uniform", "nnz": int(nnz_total), "rows_per_rank": int(A.m), "agg": int(info["agg"]),
                        "lambda": lam, "gen_s": gen_s, "build_s": info["build_seconds"],
                        "n_panels": int(info["n_panels"]),
-                       "parallelism": f"row-shard x{world}, " + ("NCCL all-reduce + all-gather per step" if args.no_overlap
-                                      else "NCCL all-reduce + per-owner broadcasts overlapped with column panels")},
+                       "exchange": args.exchange,
+                       "parallelism": f"row-shard x{world}, " + {
+                           "fused": "one fused finalize+exchange kernel per step over peer memory (CUDA IPC / NVLink), device flags",
+                           "nccl": "NCCL all-reduce + all-gather per step",
+                           "overlap": "NCCL all-reduce + per-owner broadcasts overlapped with column panels"}[
+                               "nccl" if args.no_overlap else args.exchange]},
             "roofline": {"bound": "hbm", "achieved": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9 / peak,
                          "traffic": ncu_traffic("uniform", args.dtype), "kernel": "cb_spmv_kernel",
                          "kernel_ms": kernel_ms, "peak_source": peak_src},
-            "gpu_launches": int(args.steps * (2 + (1 if args.no_overlap else info["n_panels"]))),
+            "gpu_launches": int(args.steps * ((3 + info["n_panels"]) if args.exchange == "fused" else
+                                              (2 + (1 if args.no_overlap else info["n_panels"])))),
             "clocks": clk.summary(), "cpu_baseline": None,
             "e2e": None,
         }
         print(json.dumps(line), flush=True)
+    if fused is not None:
+        if world > 1:
+            tdist.barrier()  # no peer still stores into a mapping we are about to free
+        fused.destroy()
     cb.destroy(h)
     if world > 1:
         tdist.destroy_process_group()
@@ -489,6 +508,9 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32", "f32f64"])
     ap.add_argument("--impl", default="cb", choices=["cb", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "overlap", "nccl"],
+                    help="power iteration (--config uniform): fused peer-memory exchange kernel (default), "
+                         "NCCL broadcasts overlapped with column panels, or plain NCCL all-reduce + all-gather")
     ap.add_argument("--no-overlap", action="store_true",
                     help="uniform power iteration: plain all-gather instead of per-owner broadcasts + panels")
     args = ap.parse_args()

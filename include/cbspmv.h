@@ -259,6 +259,53 @@ cbspmv_status_t cbspmv_load(const char *path, const cbspmv_options_t *opts, void
 /* Free everything the handle owns.  NULL-safe. */
 cbspmv_status_t cbspmv_destroy(cbspmv_handle_t h);
 
+/* ---------------------------------------------------------------------------------------------
+ * Fused finalize + exchange of the iterated SpMV over peer memory (
+ * BASELINE configs[4]: power iteration with rows sharded across the GPUs of one
+ * node and x replicated; the exchange is the only communication the method needs, P:433 makes
+ * block rows independent).  One context per rank.  Its single device allocation holds the two
+ * iterate buffers X[0], X[1] (n values of the dtype's x type each), the per-rank flags and the
+ * sum-of-squares partials; peers map it (CUDA IPC between processes, or plain device pointers
+ * when several "ranks" share one process) and store into it directly over NVLink.
+ *
+ * Step k of rank r (rows [r0, r0 + len)), all on one stream:
+ *   k >= 1: cbspmv_xchg_wait(seq = k)        -> sumsq = sum_q ||y_{k-1, q}||^2 (rank order)
+ *           cbspmv_spmv_scaled(x = X[k & 1], sumsq, y = X[(k+1) & 1] + r0)
+ *           cbspmv_xchg_publish(b = (k+1) & 1, r0, len, seq = k + 1)
+ * publish is ONE kernel: it reads the slice once, stores it into every peer's X[b] at r0,
+ * reduces its sum of squares (fixed order) and, after a system-scope fence, writes the partial
+ * into every peer and releases flag[r] = seq there.  No host round trip, no NCCL.
+ * Ownership: the context owns its allocation and the IPC mappings it opened; destroy frees
+ * them (after a device synchronise).  Errors: EINVAL (arguments, world > 8, unconnected
+ * peers), ENOMEM, ECUDA.  A wait that times out (a peer never published) leaves sumsq
+ * unchanged and sets the flag read by cbspmv_xchg_status. */
+#define CBSPMV_IPC_HANDLE_BYTES 64
+typedef struct cbspmv_xchg_s *cbspmv_xchg_t;
+
+/* Allocate rank `rank` of `world` (1..8) on `device` for iterates of n values (float for
+ * CBSPMV_F32, else double); flags and partials zeroed, X[0] / X[1] uninitialised. */
+cbspmv_status_t cbspmv_xchg_create(int64_t n, cbspmv_dtype_t dtype, int32_t world, int32_t rank, int32_t device,
+                                   cbspmv_xchg_t *out);
+/* The allocation's CUDA IPC handle (CBSPMV_IPC_HANDLE_BYTES bytes) for peers in other processes. */
+cbspmv_status_t cbspmv_xchg_ipc_handle(cbspmv_xchg_t x, void *handle_out);
+/* Device base pointer of the allocation (peers in the same process pass it to connect). */
+void *cbspmv_xchg_base(cbspmv_xchg_t x);
+/* Map every peer q != rank: peer_bases[q] if non-NULL (same process), else open
+ * ipc_handles + q * CBSPMV_IPC_HANDLE_BYTES (world handles, this rank's entry ignored). */
+cbspmv_status_t cbspmv_xchg_connect(cbspmv_xchg_t x, void *const *peer_bases, const void *ipc_handles);
+/* Device pointer of iterate buffer b (0 or 1), n values. */
+void *cbspmv_xchg_buffer(cbspmv_xchg_t x, int32_t b);
+/* The fused finalize + all-gather described above; seq >= 1 (= the step number + 1). */
+cbspmv_status_t cbspmv_xchg_publish(cbspmv_xchg_t x, int32_t b, int64_t r0, int64_t len, uint64_t seq,
+                                    void *stream);
+/* Device-side wait (system-scope acquire, bounded by timeout_s; <= 0: 10 s) for every rank's
+ * flag >= seq, then *sumsq_dev = the partials of step seq - 1 summed in rank order. */
+cbspmv_status_t cbspmv_xchg_wait(cbspmv_xchg_t x, uint64_t seq, double *sumsq_dev, double timeout_s, void *stream);
+/* *timed_out = 1 if any wait so far timed out (synchronous read). */
+cbspmv_status_t cbspmv_xchg_status(cbspmv_xchg_t x, int32_t *timed_out);
+/* NULL-safe. */
+cbspmv_status_t cbspmv_xchg_destroy(cbspmv_xchg_t x);
+
 const char *cbspmv_status_string(cbspmv_status_t s);
 const char *cbspmv_last_error(void);
 int32_t cbspmv_version(void);

@@ -122,6 +122,15 @@ def lib():
             "cbspmv_status_string": ([i32], ctypes.c_char_p),
             "cbspmv_last_error": ([], ctypes.c_char_p),
             "cbspmv_version": ([], i32),
+            "cbspmv_xchg_create": ([i64, i32, i32, i32, i32, ctypes.POINTER(H)], i32),
+            "cbspmv_xchg_ipc_handle": ([H, vp], i32),
+            "cbspmv_xchg_base": ([H], vp),
+            "cbspmv_xchg_connect": ([H, vp, vp], i32),
+            "cbspmv_xchg_buffer": ([H, i32], vp),
+            "cbspmv_xchg_publish": ([H, i32, i64, i64, ctypes.c_uint64, vp], i32),
+            "cbspmv_xchg_wait": ([H, ctypes.c_uint64, vp, ctypes.c_double, vp], i32),
+            "cbspmv_xchg_status": ([H, ctypes.POINTER(i32)], i32),
+            "cbspmv_xchg_destroy": ([H], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -371,3 +380,81 @@ def load(path, device: int = 0, stream=None, **opts) -> Handle:
 
 def version() -> int:
     return lib().cbspmv_version()
+
+
+# ----------------------------------------------------------------------------- peer exchange
+IPC_HANDLE_BYTES = 64
+
+
+class Exchange:
+    """cbspmv_xchg_*: one rank's iterate buffers + flags for the fused finalize / exchange of the
+    power iteration over peer memory (include/cbspmv.h).
+    ``buffer(b)`` is a torch view of iterate buffer b (n values, device ``device``)."""
+
+    def __init__(self, n: int, dtype="f64", world: int = 1, rank: int = 0, device: int = 0):
+        raw = ctypes.c_void_p()
+        self.dtype, self.n, self.world, self.rank, self.device = DTYPES[dtype], int(n), int(world), int(rank), int(device)
+        _check(lib().cbspmv_xchg_create(self.n, self.dtype, self.world, self.rank, self.device, ctypes.byref(raw)),
+               "cbspmv_xchg_create")
+        self.raw = raw
+        self._bufs = {}
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(lib().cbspmv_xchg_ipc_handle(self.raw, buf), "cbspmv_xchg_ipc_handle")
+        return buf.raw
+
+    def base(self) -> int:
+        return lib().cbspmv_xchg_base(self.raw)
+
+    def connect(self, peer_bases=None, ipc_handles=None) -> None:
+        """peer_bases: list of device pointers (same process; None entries are opened from
+        ipc_handles); ipc_handles: list of ``world`` 64-byte handles."""
+        pb = None
+        if peer_bases is not None:
+            pb = (ctypes.c_void_p * self.world)(*[p or None for p in peer_bases])
+        hb = None
+        if ipc_handles is not None:
+            hb = ctypes.create_string_buffer(b"".join(h if h else bytes(IPC_HANDLE_BYTES) for h in ipc_handles))
+        _check(lib().cbspmv_xchg_connect(self.raw, pb, hb), "cbspmv_xchg_connect")
+
+    def buffer(self, b: int):
+        import torch
+        if b not in self._bufs:
+            ptr = lib().cbspmv_xchg_buffer(self.raw, int(b))
+            if not ptr:
+                raise CBSpMVError(1, "cbspmv_xchg_buffer")
+            tdt = torch.float32 if self.dtype == F32 else torch.float64
+            self._bufs[b] = _device_view(ptr, self.n, tdt, self.device)
+        return self._bufs[b]
+
+    def publish(self, b: int, r0: int, length: int, seq: int, stream=None) -> None:
+        _check(lib().cbspmv_xchg_publish(self.raw, int(b), int(r0), int(length), int(seq),
+                                         _stream(stream, self.device)), "cbspmv_xchg_publish")
+
+    def wait(self, seq: int, sumsq_dev, timeout_s: float = 10.0, stream=None) -> None:
+        _check(lib().cbspmv_xchg_wait(self.raw, int(seq), _ptr(sumsq_dev), float(timeout_s),
+                                      _stream(stream, self.device)), "cbspmv_xchg_wait")
+
+    def timed_out(self) -> bool:
+        v = ctypes.c_int32()
+        _check(lib().cbspmv_xchg_status(self.raw, ctypes.byref(v)), "cbspmv_xchg_status")
+        return bool(v.value)
+
+    def destroy(self) -> None:
+        if self.raw:
+            self._bufs.clear()
+            lib().cbspmv_xchg_destroy(self.raw)
+            self.raw = None
+
+
+def _device_view(ptr: int, n: int, tdt, device: int):
+    """A torch tensor over n values of device memory owned by the library (no copy)."""
+    import torch
+
+    class _Arr:
+        def __init__(self):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4" if tdt == torch.float32 else "<f8",
+                                             "data": (ptr, False), "version": 3, "strides": None}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Arr(), device=f"cuda:{device}")

@@ -75,6 +75,11 @@ struct SubCsr {
 
 }  // namespace
 
+int cb_set_error(int st, const std::string &msg) {  // for the other translation units (exchange.cu)
+  g_err = msg;
+  return st;
+}
+
 struct cbspmv_s {
   int device = -1;
   int dtype = CBSPMV_F64;

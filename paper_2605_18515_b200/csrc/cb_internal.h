@@ -210,3 +210,5 @@ int cb_configure(CbDevice *dev, std::string *err);
 int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *sumsq, bool zero_y,
                    void *stream, std::string *err);
 int cb_launch_sumsq(const void *v, int64_t len, int dtype, double *out, void *stream, std::string *err);
+// Record msg as cbspmv_last_error() and return st (capi.cpp owns the thread-local string).
+int cb_set_error(int st, const std::string &msg);

@@ -213,3 +213,103 @@ def power_iteration_overlapped(h, x0, steps: int, world: int = 1, rank: int = 0,
     ss = torch.zeros(1, dtype=torch.float64, device=x0.device)
     cb.sumsq(xa, ss, device=dev)
     return it.run(xa, xb, ss, steps, on_step=on_step)
+
+
+class PeerPowerIteration:
+    """NEXT-1 (ii): the power-iteration exchange as one fused kernel over peer memory.
+
+    Same recurrence as ``PowerIteration``.  Every rank holds the two iterate buffers X[0], X[1].
+    Step k: wait for flag k (every rank published step k-1; the wait also sums the ranks'
+    partials of ||y_{k-1}||^2 in rank order), y_k = A_r (X[k&1] / ||.||) straight into the
+    rank's own slice of X[(k+1)&1], then ``publish`` stores that slice into every peer's
+    X[(k+1)&1], sends its partial sum of squares and releases flag k+1 -- all in one kernel
+    (``cbspmv_xchg_publish``); no all-reduce, no all-gather, no host round trip.  The step
+    counter k is global to the buffers (flags only grow): a run may continue or restart at k0,
+    the first step of a run taking its x and sumsq from the caller instead of a wait.
+
+    Injected ops (device: ``FusedPowerIteration``; CPU tests: numpy + gloo emulation):
+    ``spmv_scaled(x, sumsq, y)``, ``publish(b, r0, length, seq)``, ``wait(seq, sumsq)``."""
+
+    def __init__(self, spmv_scaled, publish, wait, row_bounds, rank):
+        self.spmv_scaled, self.publish, self.wait = spmv_scaled, publish, wait
+        self.row_bounds = [(int(a), int(b)) for a, b in row_bounds]
+        self.rank = rank
+
+    def run(self, X, sumsq, steps: int, on_step=None, k0: int = 0):
+        """X: the two iterate buffers with x_{k0} in X[k0 & 1]; sumsq: ||x_{k0}||^2.
+        Returns (x_{k0+steps}, sumsq), complete on every rank."""
+        r0, r1 = self.row_bounds[self.rank]
+        for k in range(k0, k0 + steps):
+            if k > k0:
+                self.wait(k, sumsq)
+            cur, nxt = X[k & 1], X[(k + 1) & 1]
+            self.spmv_scaled(cur, sumsq, nxt[r0:r1])
+            self.publish((k + 1) & 1, r0, r1 - r0, k + 1)
+            if on_step is not None:
+                self.wait(k + 1, sumsq)  # debugging / tests: a complete iterate costs the overlap
+                on_step(k - k0, nxt, sumsq)
+        if steps:
+            self.wait(k0 + steps, sumsq)
+        return X[(k0 + steps) & 1], sumsq
+
+
+class FusedPowerIteration:
+    """``PeerPowerIteration`` on the device.  The iterate buffers and flags live in one
+    ``cbspmv_xchg`` context per rank whose allocation every peer maps through CUDA IPC (handles
+    exchanged once with ``all_gather_object``); per step one ``cbspmv_spmv_scaled`` and one
+    fused ``cbspmv_xchg_publish``, the next step gated on the device by ``cbspmv_xchg_wait``.
+    Equal row shards of a square matrix.  ``run(x0, steps)`` restarts from x0 (replicated) and
+    returns (x, sumsq); x is a view of a context buffer, valid until the next run / destroy."""
+
+    def __init__(self, h, n: int, dtype="f64", world: int = 1, rank: int = 0, device: int = 0, group=None,
+                 timeout_s: float = 30.0):
+        import torch
+        import torch.distributed as tdist
+
+        import paper_2605_18515_b200 as cb
+        self.h, self.world, self.rank, self.device = h, world, rank, device
+        self.xc = cb.Exchange(n, dtype, world, rank, device)
+        if world > 1:
+            handles = [None] * world
+            tdist.all_gather_object(handles, self.xc.ipc_handle(), group=group)
+            self.xc.connect(ipc_handles=handles)
+        else:
+            self.xc.connect(peer_bases=[self.xc.base()])
+        self.X = [self.xc.buffer(0), self.xc.buffer(1)]
+        self.ss = torch.zeros(1, dtype=torch.float64, device=f"cuda:{device}")
+        m_local = h.info["m"]
+        xc = self.xc
+        self.it = PeerPowerIteration(
+            spmv_scaled=lambda x, s, y: cb.spmv_scaled(h, x, s, y),
+            publish=lambda b, r0, ln, seq: xc.publish(b, r0, ln, seq),
+            wait=lambda seq, s: xc.wait(seq, s, timeout_s),
+            row_bounds=[(r * m_local, (r + 1) * m_local) for r in range(world)], rank=rank)
+        self.k = 0
+        torch.cuda.synchronize(device)
+        if world > 1:
+            tdist.barrier(group=group)  # every peer mapped before anyone stores into it
+
+    def run(self, x0, steps: int, on_step=None):
+        import paper_2605_18515_b200 as cb
+        # safe to overwrite X[k & 1]: every peer's last store into it preceded our last wait(k)
+        self.X[self.k & 1].copy_(x0)
+        cb.sumsq(self.X[self.k & 1], self.ss, device=self.device)
+        x, ss = self.it.run(self.X, self.ss, steps, on_step=on_step, k0=self.k)
+        self.k += steps
+        return x, ss
+
+    def timed_out(self) -> bool:
+        return self.xc.timed_out()
+
+    def destroy(self) -> None:
+        self.xc.destroy()
+
+
+def power_iteration_fused(h, x0, steps: int, world: int = 1, rank: int = 0, group=None, on_step=None,
+                          timeout_s: float = 30.0):
+    """One-shot ``FusedPowerIteration``: returns (x, sumsq, driver); call ``driver.destroy()``
+    when x (a view of its buffer) is no longer needed."""
+    f = FusedPowerIteration(h, x0.numel(), {4: "f32", 8: "f64"}[x0.element_size()], world, rank,
+                            x0.device.index, group, timeout_s)
+    x, ss = f.run(x0, steps, on_step=on_step)
+    return x, ss, f

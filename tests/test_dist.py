@@ -236,3 +236,87 @@ def test_panel_power_iteration_overlap_matches_recurrence(world, P):
         assert np.isclose(ss_r, ss, rtol=1e-12)
         assert np.allclose(x_r, x, rtol=1e-11)  # every rank ends with the complete iterate
         assert ran == order and own_first
+
+
+def _peer_pi_worker(rank, world, port, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 1024 * world
+        A = synth.uniform(n, n, 30, 53, val_mode=1)
+        m_loc = n // world
+        S = cbd.slice_rows(A, rank * m_loc, (rank + 1) * m_loc)
+        X = [torch.ones(n, dtype=torch.float64), torch.full((n,), float("nan"), dtype=torch.float64)]
+        partials = np.full((2, world), np.nan)  # the context's partials[parity][rank]
+        flags = [0] * world
+        calls = []
+
+        def spmv_scaled(x, ss, y):  # oracle stand-in for cbspmv_spmv_scaled
+            calls.append(("spmv", float(ss.item())))
+            y.copy_(torch.from_numpy(oracle.spmv_csr(S, x.numpy() / np.sqrt(ss.item()))[0]))
+
+        def publish(b, r0, length, seq):  # emulates cbspmv_xchg_publish: slice -> every peer's X[b]
+            calls.append(("publish", b, seq))
+            mine = X[b][r0:r0 + length].clone()
+            parts = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(parts, mine)
+            X[b].copy_(torch.cat(parts))
+            tot = torch.tensor([float(torch.dot(mine, mine))], dtype=torch.float64)
+            allp = [torch.empty_like(tot) for _ in range(world)]
+            dist.all_gather(allp, tot)
+            partials[(seq - 1) & 1] = [float(t.item()) for t in allp]
+            for r in range(world):
+                flags[r] = seq
+
+        def wait(seq, ss):  # emulates cbspmv_xchg_wait: flags >= seq, partials summed in rank order
+            calls.append(("wait", seq))
+            assert min(flags) >= seq
+            s = 0.0
+            for r in range(world):
+                s += partials[(seq - 1) & 1][r]
+            ss.fill_(s)
+
+        it = cbd.PeerPowerIteration(spmv_scaled, publish, wait,
+                                    row_bounds=[(r * m_loc, (r + 1) * m_loc) for r in range(world)], rank=rank)
+        ss = torch.tensor([float(n)], dtype=torch.float64)
+        x, ss = it.run(X, ss, steps)
+        q.put((rank, float(ss.item()), x.numpy().copy(), calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_power_iteration_protocol_matches_recurrence(world):
+    """NEXT-1 (ii) host logic: wait(k) -> spmv into X[(k+1)&1] -> publish(seq k+1), double buffers
+    and partial parities, == the plain recurrence on every rank."""
+    steps = 9
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_peer_pi_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 1024 * world
+    d = synth.uniform(n, n, 30, 53, val_mode=1).to_dense()
+    x = np.ones(n)
+    ss = float(n)
+    for _ in range(steps):
+        y = d @ (x / np.sqrt(ss))
+        ss = float(y @ y)
+        x = y
+    expect = []
+    for k in range(steps):
+        if k:
+            expect.append(("wait", k))
+        expect.append("spmv")
+        expect.append(("publish", (k + 1) & 1, k + 1))
+    expect.append(("wait", steps))
+    for rank, ss_r, x_r, calls in res:
+        assert np.isclose(ss_r, ss, rtol=1e-12)
+        assert np.allclose(x_r, x, rtol=1e-11)
+        assert [c if c[0] != "spmv" else "spmv" for c in calls] == expect
+    assert len({r[1] for r in res}) == 1  # partials summed in rank order: the same bits everywhere

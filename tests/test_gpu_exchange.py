@@ -1,0 +1,196 @@
+"""GPU tests of the fused finalize + exchange over peer memory (SURVEY §8(f) NEXT-1 (ii),
+include/cbspmv.h cbspmv_xchg_*): the power iteration of BASELINE configs[4] with the y shards
+pushed into every peer's next iterate by one kernel and the next step gated by device flags.
+
+This run has one GPU, so the peers are (a) P contexts in one process on cuda:0, connected by
+plain device pointers and interleaved on one stream, and (b) two processes on cuda:0 connected
+through CUDA IPC, each spinning on the other's flags.  Both must reproduce the recurrence the
+NCCL path computes (``dist.power_iteration_device`` at N = 1, whose steps are pinned to the
+oracle in test_gpu_parity.py) to within the fp64 bar, every rank holding the same bits.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2605_18515_b200 as cb
+import synth
+from paper_2605_18515_b200 import dist as cbd
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _ok():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _reference(A, steps, dtype=torch.float64):
+    """The NCCL-path driver at N = 1 on the whole matrix (its steps are oracle-pinned)."""
+    h = cb.build(A, dtype="f64" if dtype == torch.float64 else "f32", device=0)
+    x, ss = cbd.power_iteration_device(h, torch.ones(A.n, dtype=dtype, device=DEV), steps)
+    torch.cuda.synchronize()
+    out = x.cpu().numpy().copy(), float(ss.item())
+    cb.destroy(h)
+    return out
+
+
+def _simulated_ranks(A, P, steps, dtype="f64"):
+    """P ranks in one process on one GPU, run step-interleaved on one stream."""
+    m_loc = A.m // P
+    bounds = [(r * m_loc, (r + 1) * m_loc) for r in range(P)]
+    hs = [cb.build(cbd.slice_rows(A, a, b), dtype=dtype, device=0) for a, b in bounds]
+    xcs = [cb.Exchange(A.n, dtype, P, r, 0) for r in range(P)]
+    bases = [xc.base() for xc in xcs]
+    for xc in xcs:
+        xc.connect(peer_bases=bases)
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    sss = []
+    for xc in xcs:
+        xc.buffer(0).fill_(1.0)
+        xc.buffer(1).fill_(float("nan"))  # every slice must be overwritten by its owner's publish
+        ss = torch.zeros(1, dtype=torch.float64, device=DEV)
+        cb.sumsq(xc.buffer(0), ss)
+        sss.append(ss)
+    for k in range(steps):
+        for r, (a, b) in enumerate(bounds):
+            if k:
+                xcs[r].wait(k, sss[r], timeout_s=5.0)
+            cb.spmv_scaled(hs[r], xcs[r].buffer(k & 1), sss[r], xcs[r].buffer((k + 1) & 1)[a:b])
+            xcs[r].publish((k + 1) & 1, a, b - a, k + 1)
+    for r in range(P):
+        xcs[r].wait(steps, sss[r], timeout_s=5.0)
+    torch.cuda.synchronize()
+    assert not any(xc.timed_out() for xc in xcs)
+    xs = [xc.buffer(steps & 1).to(tdt).cpu().numpy().copy() for xc in xcs]
+    ss = [float(s.item()) for s in sss]
+    for h in hs:
+        cb.destroy(h)
+    for xc in xcs:
+        xc.destroy()
+    return xs, ss
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_fused_exchange_simulated_ranks_match_recurrence(P):
+    _ok()
+    n = 2048 * P
+    A = synth.uniform(n, n, 40, 61, val_mode=1)  # values U(0,1]: converging power iteration
+    steps = 12
+    x_ref, ss_ref = _reference(A, steps)
+    xs, ss = _simulated_ranks(A, P, steps)
+    assert len(set(ss)) == 1  # partials summed in rank order: identical bits on every rank
+    assert np.isclose(ss[0], ss_ref, rtol=1e-13)
+    for x in xs:
+        assert np.array_equal(x, xs[0])  # every rank holds the complete, identical iterate
+        assert np.allclose(x, x_ref, rtol=1e-12, atol=0)
+
+
+def test_fused_exchange_all_ones_fixed_point():
+    """Uniform all-ones, 50 per row: lambda = 50 at every step (SURVEY §8(c) closed form)."""
+    _ok()
+    n = 4096
+    A = synth.uniform(n, n, 50, 62, val_mode=3)
+    xs, ss = _simulated_ranks(A, 4, 20)
+    assert np.allclose(np.sqrt(ss), 50.0, rtol=1e-15, atol=0)
+    assert np.allclose(xs[0], xs[0][0], rtol=1e-15)  # the normalised ones vector (up to rounding)
+
+
+def test_fused_exchange_f32():
+    _ok()
+    n = 4096
+    A = synth.uniform(n, n, 40, 63, val_mode=1)
+    x_ref, ss_ref = _reference(A, 8, torch.float32)
+    xs, ss = _simulated_ranks(A, 2, 8, dtype="f32")
+    assert len(set(ss)) == 1
+    assert np.isclose(ss[0], ss_ref, rtol=1e-5)
+    assert np.allclose(xs[0], x_ref, rtol=1e-5)
+
+
+def test_fused_exchange_wait_times_out_without_publisher():
+    """A rank whose peer never publishes: the device wait gives up (bounded spin), flags it, and
+    leaves sumsq untouched -- no hang."""
+    _ok()
+    xcs = [cb.Exchange(64, "f64", 2, r, 0) for r in range(2)]
+    xcs[0].connect(peer_bases=[xc.base() for xc in xcs])
+    ss = torch.full((1,), 7.0, dtype=torch.float64, device=DEV)
+    xcs[0].wait(1, ss, timeout_s=0.05)
+    torch.cuda.synchronize()
+    assert xcs[0].timed_out() and float(ss.item()) == 7.0
+    for xc in xcs:
+        xc.destroy()
+
+
+def test_fused_exchange_argument_errors():
+    _ok()
+    with pytest.raises(cb.CBSpMVError):
+        cb.Exchange(16, "f64", 9, 0, 0)  # world > 8
+    xc = cb.Exchange(16, "f64", 2, 0, 0)
+    with pytest.raises(cb.CBSpMVError):
+        xc.publish(1, 0, 16, 1)  # peer 1 not connected
+    xc.connect(peer_bases=[xc.base(), xc.base()])
+    with pytest.raises(cb.CBSpMVError):
+        xc.publish(1, 8, 16, 1)  # slice past n
+    with pytest.raises(cb.CBSpMVError):
+        xc.publish(1, 0, 8, 0)  # seq 0 is reserved (flags start at 0)
+    xc.destroy()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ipc_worker(rank, world, port, steps, q):
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)  # handle exchange + barrier only
+    try:
+        torch.cuda.set_device(0)
+        n = 4096 * world
+        A = synth.uniform(n, n, 40, 64, val_mode=1)
+        m_loc = n // world
+        h = cb.build(cbd.slice_rows(A, rank * m_loc, (rank + 1) * m_loc), device=0)
+        x0 = torch.ones(n, dtype=torch.float64, device=DEV)
+        x, ss, xc = cbd.power_iteration_fused(h, x0, steps, world, rank, timeout_s=20.0)
+        torch.cuda.synchronize()
+        first = x.cpu().numpy().copy()
+        x, ss = xc.run(x0, steps)  # restart on the same buffers: flags keep growing
+        torch.cuda.synchronize()
+        assert np.allclose(x.cpu().numpy(), first, rtol=1e-13, atol=0)  # fp64 RED order may differ
+        q.put((rank, xc.timed_out(), float(ss.item()), first))
+        tdist.barrier()  # nobody unmaps while a peer may still store into it
+        xc.destroy()
+        cb.destroy(h)
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_fused_exchange_two_processes_ipc():
+    """Two processes on cuda:0 mapping each other's iterate buffers through CUDA IPC."""
+    _ok()
+    import torch.multiprocessing as mp
+    steps, world = 10, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = 4096 * world
+    x_ref, ss_ref = _reference(synth.uniform(n, n, 40, 64, val_mode=1), steps)
+    for rank, timed_out, ss, x in res:
+        assert not timed_out
+        assert ss == res[0][2]
+        assert np.isclose(ss, ss_ref, rtol=1e-13)
+        assert np.allclose(x, x_ref, rtol=1e-12, atol=0)
