@@ -124,6 +124,23 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+# Random x-gather ceiling measured on this pool's B200 (tools/mb_mixed.cu,
+# profiles/r1_microbench_tma_mixed.txt): ~0.94 random 32-byte sector requests per SM-cycle,
+# whether issued by LDG or TMA gather4.  An aggregated matrix needs one random gather per
+# restore entry (aggregated column of a block row), so n_restore / (0.94 * SMs * clock) bounds
+# its SpMV from below independently of HBM.
+GATHER_REQ_PER_SM_CYCLE = 0.94
+
+
+def gather_floor(info, kernel_ms, sms=148, mhz=1965.0):
+    if not info["agg"]:
+        return None
+    n = int(info["n_restore"])
+    floor_ms = n / (GATHER_REQ_PER_SM_CYCLE * sms * mhz * 1e6) * 1e3
+    return {"x_gathers": n, "floor_ms": floor_ms, "frac": floor_ms / kernel_ms if kernel_ms else None,
+            "basis": "0.94 random sector requests / SM-cycle (profiles/r1_microbench_tma_mixed.txt), 148 SMs, 1965 MHz"}
+
+
 def ncu_traffic(config: str, dtype: str):
     """dram bytes per launch of the SpMV kernel from the committed ncu --set full capture, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -296,7 +313,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
                 "achieved_hbm_gbs_step": info["alg_bytes"] / (ms * 1e-3) / 1e9,
                 "tb_load_sd": info["tb_load_sd"], "tb_load_sd_natural": info["tb_load_sd_natural"],
                 "gen_s": gen_s, "build_s": info["build_seconds"], "upload_s": info["upload_seconds"],
-                "grid": info["grid"], "also": also,
+                "grid": info["grid"], "gather_floor": gather_floor(info, kernel_ms), "also": also,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "cb_spmv_kernel",
@@ -354,6 +371,7 @@ def measure_also(names, dtype, steps, warmup, local_rank):
                      "gflops": 2.0 * i["nnz"] / (ms * 1e-3) / 1e9, "ms_per_step": ms, "kernel_ms": kms,
                      "alg_bytes": int(i["alg_bytes"]),
                      "hbm_frac": i["alg_bytes"] / (kms * 1e-3) / 1e9 / peak,
+                     "gather_floor": gather_floor(i, kms),
                      "l2_resident": i["alg_bytes"] < 126e6}
         cb.destroy(h)
         del A
@@ -431,7 +449,7 @@ def run_power(args, rank, world, local_rank):
             "config": {"workload": "BASELINE configs[4]: power iteration on uniform 2^25 x 2^25, 50 nnz/row",
                        "name": "uniform", "nnz": int(nnz_total), "rows_per_rank": int(A.m), "agg": int(info["agg"]),
                        "lambda": lam, "gen_s": gen_s, "build_s": info["build_seconds"],
-                       "n_panels": int(info["n_panels"]),
+                       "n_panels": int(info["n_panels"]), "gather_floor": gather_floor(info, kernel_ms),
                        "exchange": args.exchange,
                        "parallelism": f"row-shard x{world}, " + {
                            "fused": "one fused finalize+exchange kernel per step over peer memory (CUDA IPC / NVLink), device flags",
