@@ -179,6 +179,16 @@ cbspmv_status_t cbspmv_panel_bounds(cbspmv_handle_t h, int32_t k, int64_t *c0, i
  * and synchronises the stream before returning. */
 cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_host, void *stream);
 
+/* End to end over `count` independent right-hand sides (a batch of requests served from host
+ * memory): y_host[k] := A·x_host[k], k = 0..count-1 (n and m values each).  Pipelined over two
+ * device staging slots with the library's own copy streams: the upload of x_{k+1} and the
+ * download of y_{k-1} overlap the SpMV of x_k on `stream`.  Host buffers must stay valid and
+ * unmodified until the call returns (it synchronises); pinned memory is needed for the copies
+ * to overlap (pageable memory works, serialised).  The same x / y pointer may repeat across k.
+ * Errors: EINVAL, EUNSUPPORTED (host-only handle), ENOMEM, ECUDA. */
+cbspmv_status_t cbspmv_spmv_host_batch(cbspmv_handle_t h, const void *const *x_host, void *const *y_host,
+                                       int64_t count, void *stream);
+
 /* *out_dev (one double on the device) := sum_i v_i^2 over len vector values of dtype
  * (float for CBSPMV_F32, else double; the power-iteration finalize step). */
 cbspmv_status_t cbspmv_sumsq(const void *v_dev, int64_t len, cbspmv_dtype_t dtype, double *out_dev,

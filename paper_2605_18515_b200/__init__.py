@@ -103,6 +103,7 @@ def lib():
             "cbspmv_spmv_add": ([H, vp, vp, vp], i32),
             "cbspmv_spmv_scaled": ([H, vp, vp, vp, vp], i32),
             "cbspmv_spmv_host": ([H, vp, vp, vp], i32),
+            "cbspmv_spmv_host_batch": ([H, vp, vp, i64, vp], i32),
             "cbspmv_spmv_panel": ([H, i32, vp, vp, vp, i32, vp], i32),
             "cbspmv_panel_bounds": ([H, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
             "cbspmv_sumsq": ([vp, i64, i32, vp, i32, vp], i32),
@@ -287,6 +288,22 @@ def spmv_host(h: Handle, x: np.ndarray, y: np.ndarray, stream=None) -> None:
         raise ValueError("size mismatch")
     _check(lib().cbspmv_spmv_host(h.raw, x.ctypes.data, y.ctypes.data, _stream(stream, h.device)),
            "cbspmv_spmv_host")
+
+
+def spmv_host_batch(h: Handle, xs, ys, stream=None) -> None:
+    """cbspmv_spmv_host_batch: ys[k] := A xs[k] for host arrays (pinned for overlap), pipelined."""
+    if len(xs) != len(ys):
+        raise ValueError("xs and ys differ in length")
+    vt = vector_dtype(h.dtype)
+    for x, y in zip(xs, ys):
+        if x.dtype != vt or y.dtype != vt or x.size != h.info["n"] or y.size != h.info["m"]:
+            raise ValueError("x / y host arrays must match the handle's dtype and shape")
+        if not (x.flags.c_contiguous and y.flags.c_contiguous and y.flags.writeable):
+            raise ValueError("x / y must be C-contiguous (y writeable)")
+    k = len(xs)
+    xp = (ctypes.c_void_p * max(1, k))(*[x.ctypes.data for x in xs])
+    yp = (ctypes.c_void_p * max(1, k))(*[y.ctypes.data for y in ys])
+    _check(lib().cbspmv_spmv_host_batch(h.raw, xp, yp, k, _stream(stream, h.device)), "cbspmv_spmv_host_batch")
 
 
 def sumsq(v, out, device: int = 0, stream=None) -> None:

@@ -90,6 +90,10 @@ struct cbspmv_s {
   cbspmv_info_t info{};
   void *d_x_tmp = nullptr;
   void *d_y_tmp = nullptr;
+  // cbspmv_spmv_host_batch: second x / y staging slot, copy streams and slot events
+  void *d_x_tmp2 = nullptr, *d_y_tmp2 = nullptr;
+  cudaStream_t s_up = nullptr, s_down = nullptr;
+  cudaEvent_t ev_up[2] = {}, ev_done[2] = {}, ev_down[2] = {};
 };
 
 extern "C" {
@@ -128,6 +132,18 @@ static void free_device(cbspmv_s *h) {
   cudaFree(h->d_x_tmp);
   cudaFree(h->d_y_tmp);
   h->d_x_tmp = nullptr; h->d_y_tmp = nullptr;
+  cudaFree(h->d_x_tmp2);
+  cudaFree(h->d_y_tmp2);
+  h->d_x_tmp2 = nullptr; h->d_y_tmp2 = nullptr;
+  for (int b = 0; b < 2; b++) {
+    if (h->ev_up[b]) cudaEventDestroy(h->ev_up[b]);
+    if (h->ev_done[b]) cudaEventDestroy(h->ev_done[b]);
+    if (h->ev_down[b]) cudaEventDestroy(h->ev_down[b]);
+    h->ev_up[b] = h->ev_done[b] = h->ev_down[b] = nullptr;
+  }
+  if (h->s_up) cudaStreamDestroy(h->s_up);
+  if (h->s_down) cudaStreamDestroy(h->s_down);
+  h->s_up = h->s_down = nullptr;
 }
 
 // Device page stream of one panel's canonical format, uploaded in one copy (a8).
@@ -456,6 +472,63 @@ cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_
   int st = launch_all(h, h->d_x_tmp, h->d_y_tmp, nullptr, true, stream, &err);
   if (st != CBSPMV_OK) return fail(st, err);
   if (yb) e = cudaMemcpyAsync(y_host, h->d_y_tmp, yb, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ECUDA, cudaGetErrorString(e)); }
+  return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_spmv_host_batch(cbspmv_handle_t h, const void *const *x_host, void *const *y_host,
+                                       int64_t count, void *stream) {
+  if (!h) return fail(CBSPMV_EINVAL, "null handle");
+  if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle");
+  if (count < 0 || (count > 0 && (!x_host || !y_host))) return fail(CBSPMV_EINVAL, "bad batch arguments");
+  for (int64_t k = 0; k < count; k++)
+    if ((h->info.n > 0 && !x_host[k]) || (h->info.m > 0 && !y_host[k])) return fail(CBSPMV_EINVAL, "null x or y");
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaSuccess;
+  const size_t xb = (size_t)h->info.n * h->vec_size, yb = (size_t)h->info.m * h->vec_size;
+  if (!h->d_x_tmp && xb) e = cudaMalloc(&h->d_x_tmp, xb);
+  if (e == cudaSuccess && !h->d_y_tmp && yb) e = cudaMalloc(&h->d_y_tmp, yb);
+  if (e == cudaSuccess && !h->d_x_tmp2 && xb) e = cudaMalloc(&h->d_x_tmp2, xb);
+  if (e == cudaSuccess && !h->d_y_tmp2 && yb) e = cudaMalloc(&h->d_y_tmp2, yb);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ENOMEM, "device x/y staging"); }
+  if (!h->s_up) {
+    e = cudaStreamCreateWithFlags(&h->s_up, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_down, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; b++) {
+      e = cudaEventCreateWithFlags(&h->ev_up[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_done[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_down[b], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ECUDA, cudaGetErrorString(e)); }
+  }
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  void *dx[2] = {h->d_x_tmp, h->d_x_tmp2}, *dy[2] = {h->d_y_tmp, h->d_y_tmp2};
+  // nothing issued before this call may still use the staging slots
+  e = cudaEventRecord(h->ev_done[0], cs);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_done[1], cs);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_down[0], cs);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_down[1], cs);
+  std::string err;
+  for (int64_t k = 0; k < count && e == cudaSuccess; k++) {
+    const int b = (int)(k & 1);
+    // upload x_k into slot b once SpMV k-2 (its last reader) is done
+    e = cudaStreamWaitEvent(h->s_up, h->ev_done[b], 0);
+    if (e == cudaSuccess && xb) e = cudaMemcpyAsync(dx[b], x_host[k], xb, cudaMemcpyHostToDevice, h->s_up);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_up[b], h->s_up);
+    // SpMV k on the caller's stream once x_k landed and y slot b was downloaded (step k-2)
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_up[b], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, h->ev_down[b], 0);
+    if (e != cudaSuccess) break;
+    int st = launch_all(h, dx[b], dy[b], nullptr, true, stream, &err);
+    if (st != CBSPMV_OK) return fail(st, err);
+    e = cudaEventRecord(h->ev_done[b], cs);
+    // download y_k behind the SpMV while the next upload / SpMV proceed
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s_down, h->ev_done[b], 0);
+    if (e == cudaSuccess && yb) e = cudaMemcpyAsync(y_host[k], dy[b], yb, cudaMemcpyDeviceToHost, h->s_down);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_down[b], h->s_down);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->s_down);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ECUDA, cudaGetErrorString(e)); }
   return CBSPMV_OK;

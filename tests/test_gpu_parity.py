@@ -473,3 +473,34 @@ def test_spmv_panel_sum_equals_spmv():
     y_ref, _ = oracle.spmv_csr(A, x)
     assert np.array_equal(y.cpu().numpy(), y_ref)  # exact-integer data: bitwise
     assert [cb.panel_bounds(h, k)[0] for k in range(4)][0] == 0 and cb.panel_bounds(h, 3)[1] == A.n
+
+
+@pytest.mark.parametrize("count", [0, 1, 2, 5])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_spmv_host_batch_pipelined(count, dtype):
+    """cbspmv_spmv_host_batch: every request's y equals the oracle's, with repeated host
+    buffers, odd counts and the two staging slots alternating."""
+    _ok()
+    A = synth.make("clustered", small=True)
+    h = cb.build(A, dtype=dtype, device=0)
+    vt = np.float32 if dtype == "f32" else np.float64
+    rel = 1e-5 if dtype == "f32" else 1e-12
+
+    def ref(x):
+        return ref32(A, x) if dtype == "f32" else oracle.spmv_csr(A, x)
+
+    xs = [synth.vector(A.n, synth.VEC_UNIFORM, seed=100 + k).astype(vt) for k in range(max(count, 1))]
+    ys = [np.full(A.m, np.nan, vt) for _ in range(max(count, 1))]
+    cb.spmv_host_batch(h, xs[:count], ys[:count])
+    for k in range(count):
+        y_ref, R = ref(xs[k].astype(np.float64))
+        check_rows(ys[k].astype(np.float64), y_ref, R, rel)
+    if count == 0:
+        assert np.isnan(ys[0]).all()
+    # the same host buffers reused across requests (a ring), as bench.py does
+    ring_y = [np.empty(A.m, vt) for _ in range(2)]
+    cb.spmv_host_batch(h, [xs[0]] * 3, [ring_y[k % 2] for k in range(3)])
+    y_ref, R = ref(xs[0].astype(np.float64))
+    for yk in ring_y:
+        check_rows(yk.astype(np.float64), y_ref, R, rel)
+    cb.destroy(h)
