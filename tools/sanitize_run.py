@@ -25,4 +25,36 @@ for A, opts in cases:
         cb.spmv_scaled(h, x, ss, y)
         torch.cuda.synchronize()
         cb.destroy(h)
+# pipelined host batch (two staging slots, copy streams)
+A = synth.clustered(1 << 11)
+h = cb.build(A, device=0)
+xs = [synth.vector(A.n, 0, k) for k in range(3)]
+ys = [np.empty(A.m) for _ in range(3)]
+cb.spmv_host_batch(h, xs, ys)
+cb.destroy(h)
+# fused finalize + exchange: 2 ranks simulated in one process, 3 steps
+from paper_2605_18515_b200 import dist as cbd  # noqa: E402
+A = synth.uniform(1 << 11, 1 << 11, 20, 6, 1)
+m2 = A.m // 2
+hs = [cb.build(cbd.slice_rows(A, r * m2, (r + 1) * m2), device=0) for r in range(2)]
+xcs = [cb.Exchange(A.n, "f64", 2, r, 0) for r in range(2)]
+for xc in xcs:
+    xc.connect(peer_bases=[c.base() for c in xcs])
+    xc.buffer(0).fill_(1.0)
+    xc.buffer(1).zero_()
+sss = [torch.tensor([float(A.n)], dtype=torch.float64, device="cuda:0") for _ in range(2)]
+for k in range(3):
+    for r in range(2):
+        if k:
+            xcs[r].wait(k, sss[r], 5.0)
+        cb.spmv_scaled(hs[r], xcs[r].buffer(k & 1), sss[r], xcs[r].buffer((k + 1) & 1)[r * m2:(r + 1) * m2])
+        xcs[r].publish((k + 1) & 1, r * m2, m2, k + 1)
+for r in range(2):
+    xcs[r].wait(3, sss[r], 5.0)
+torch.cuda.synchronize()
+assert not any(xc.timed_out() for xc in xcs)
+for h in hs:
+    cb.destroy(h)
+for xc in xcs:
+    xc.destroy()
 print("sanitize run ok")
