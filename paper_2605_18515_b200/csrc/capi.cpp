@@ -162,6 +162,17 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   CbDevice &D = P->dev;
   D.device = o.device; D.dtype = dtype; D.agg = c.agg; D.m = c.m; D.n = c.n;
   D.n_pages = npages; D.page_cap = cap;
+  // hub block rows (power-law matrices): >= 8192 stored entries in one 16-row block row.  Their
+  // rows receive ~10^4-10^5 same-address atomics per SpMV, so the kernel sums same-row runs of a
+  // COO group in the warp before the RED (R-MAT, 8 ranks: rank 0 0.47 -> 0.22 ms).  Elsewhere the
+  // extra vote / scan only costs (Laplacian 0.033 -> 0.048 ms), so it is off.
+  {
+    std::vector<int64_t> brn((size_t)std::max<int64_t>(c.blk_m, 1), 0);
+    for (int64_t i = 0; i < c.nb; i++) brn[(size_t)c.br[i]] += c.nnzb[i];
+    const int64_t mx = brn.empty() ? 0 : *std::max_element(brn.begin(), brn.end());
+    D.coo_runs = mx >= 8192;
+    if (const char *v = std::getenv("CBSPMV_COO_RUNS")) D.coo_runs = std::atoi(v) != 0;
+  }
   st = cb_configure(&D, err);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   // persistent CTA g streams pages [cta[g], cta[g+1]): equal byte shares

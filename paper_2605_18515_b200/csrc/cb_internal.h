@@ -199,6 +199,7 @@ struct CbDevice {
   int nstage = 0;
   int groups = 1;
   int consumers = 0;
+  int coo_runs = 0;  // hub block rows: sum same-row runs of a COO group before its RED
   const uint8_t *d_stream = nullptr;
   const uint64_t *d_page_off = nullptr;
   const uint32_t *d_cta_page = nullptr;  // grid + 1 page boundaries per persistent CTA

@@ -187,12 +187,36 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
 }
 
 template <typename V, bool SCALED>
-__device__ __forceinline__ void coo_finish(const CooPend<V> &r, V scale, V *__restrict__ y, Dbg dbg) {
-  if (r.valid) {
-    V p = r.v * r.xv;
-    if constexpr (SCALED) p *= scale;
-    red_add(y + r.yrow, p, dbg);
+__device__ __forceinline__ void coo_finish(const CooPend<V> &r, V scale, V *__restrict__ y, Dbg dbg, bool runs) {
+  V p = r.v * r.xv;
+  if constexpr (SCALED) p *= scale;
+  if (runs) {
+  // Runs of elements on the same y row (a COO record is sorted by (row, col)) are
+  // summed in the warp first and added by one RED from the run's first lane.  Hub rows of
+  // power-law matrices otherwise receive ~10^5 same-address atomics per SpMV, serialised in L2
+  // (R-MAT: row 0 gets 115 K).  Groups without a run skip the scan (one vote).
+  const int lane = threadIdx.x & 31;
+  const uint32_t key = r.valid ? r.yrow : 0xFFFFFFFFu - (uint32_t)lane;  // invalid lanes: unique keys
+  const uint32_t kn = __shfl_down_sync(kFull, key, 1);
+  bool tail = lane == 31 || kn != key;  // last lane of its run
+  if (__any_sync(kFull, !tail)) {
+    const uint32_t kp = __shfl_up_sync(kFull, key, 1);
+    const bool head = lane == 0 || kp != key;
+    // segmented suffix scan: v = sum of p over [lane, end of run]
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const V o = __shfl_down_sync(kFull, p, d);
+      const bool ot = __shfl_down_sync(kFull, tail, d);
+      if (!tail && lane + d < 32) {
+        p += o;
+        tail = ot;
+      }
+    }
+    if (r.valid && head) red_add(y + r.yrow, p, dbg);
+    return;
   }
+  }
+  if (r.valid) red_add(y + r.yrow, p, dbg);
 }
 
 // x tile of one block loaded by the warp itself (aggregated matrices have no gather warps):
@@ -323,7 +347,7 @@ __device__ __forceinline__ void issue_tiles(const uint4 *descs, uint32_t iw, V *
 
 // Warp roles: 0 = TMA producer, the rest = consumer groups.  M: matrix value type of the
 // records; V: type of x, y and the accumulation (M = float, V = double: the mixed variant).
-template <typename M, typename V, bool AGG, bool SCALED>
+template <typename M, typename V, bool AGG, bool SCALED, bool RUNS>
 __global__ void __launch_bounds__(kMaxThreads, 1)
     cb_spmv_kernel(KParams P, const V *__restrict__ x, V *__restrict__ y) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -379,6 +403,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   V *wscratch = scratch + cw * 16;
   const uint64_t xpol = policy_evict_last();
   const int G = P.groups, grp = cw / kGroupWarps;
+  constexpr bool runs = RUNS;  // hub block rows: same-row run sums before the COO REDs
   int s = grp % S;
   uint32_t parity = (uint32_t)((grp / S) & 1);
   for (uint32_t p = p0 + grp; p < p1; p += G) {
@@ -412,13 +437,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
 #pragma unroll
           for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V, AGG>(page, descs, iws[j], xbuf, x, lane, dbg, xpol);
 #pragma unroll
-          for (int j = 0; j < 4; j++) coo_finish<V, SCALED>(q[j], scale, y, dbg);
+          for (int j = 0; j < 4; j++) coo_finish<V, SCALED>(q[j], scale, y, dbg, runs);
         } else {
           for (int j = 0; j < nv; j++) {
             const uint32_t iw = iws[j];
             const int t = (iw >> 12) & 3;
             if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
-              coo_finish<V, SCALED>(coo_issue<M, V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
+              coo_finish<V, SCALED>(coo_issue<M, V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg, runs);
             } else {
               const uint4 dh = descs[iw & 0xFFF];
               const V *xt = warp_tile<V, AGG>(page, dh, x, wscratch, lane, dbg);
@@ -458,7 +483,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         __syncwarp();
         const int t = (iw >> 12) & 3, hb = iw & 0xFFF;
         if (t == CBSPMV_FMT_COO && !(iw >> 31)) {
-          coo_finish<V, SCALED>(coo_issue<M, V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg);
+          coo_finish<V, SCALED>(coo_issue<M, V, AGG>(page, descs, iw, xbuf, x, lane, dbg, xpol), scale, y, dbg, runs);
         } else {
           const uint4 dh = descs[hb];
           const V *xt = xbuf + hb * 16;
@@ -505,15 +530,19 @@ __global__ void cb_sumsq_kernel(const V *__restrict__ v, int64_t len, double *ou
 }
 
 template <typename M, typename V>
-const void *kernel_ptr(int agg, bool scaled) {
-  if (agg) return scaled ? (const void *)&cb_spmv_kernel<M, V, true, true> : (const void *)&cb_spmv_kernel<M, V, true, false>;
-  return scaled ? (const void *)&cb_spmv_kernel<M, V, false, true> : (const void *)&cb_spmv_kernel<M, V, false, false>;
+const void *kernel_ptr(int agg, bool scaled, bool runs) {
+  if (agg && runs)
+    return scaled ? (const void *)&cb_spmv_kernel<M, V, true, true, true> : (const void *)&cb_spmv_kernel<M, V, true, false, true>;
+  if (agg) return scaled ? (const void *)&cb_spmv_kernel<M, V, true, true, false> : (const void *)&cb_spmv_kernel<M, V, true, false, false>;
+  return scaled ? (const void *)&cb_spmv_kernel<M, V, false, true, false> : (const void *)&cb_spmv_kernel<M, V, false, false, false>;
 }
 
-const void *select_kernel(int dtype, int agg, bool scaled) {
-  if (dtype == CBSPMV_F64) return kernel_ptr<double, double>(agg, scaled);
-  if (dtype == CBSPMV_F32) return kernel_ptr<float, float>(agg, scaled);
-  return kernel_ptr<float, double>(agg, scaled);  // CBSPMV_F32F64
+// runs (in-warp same-row run sums before COO REDs) is compiled only into the aggregated kernels:
+// hub block rows come with power-law matrices, which the th0 rule aggregates
+const void *select_kernel(int dtype, int agg, bool scaled, bool runs) {
+  if (dtype == CBSPMV_F64) return kernel_ptr<double, double>(agg, scaled, runs);
+  if (dtype == CBSPMV_F32) return kernel_ptr<float, float>(agg, scaled, runs);
+  return kernel_ptr<float, double>(agg, scaled, runs);  // CBSPMV_F32F64
 }
 
 // bytes of one x / y element
@@ -560,8 +589,9 @@ int cb_configure(CbDevice *dev, std::string *err) {
   dev->consumers = groups * kGroupWarps;
   for (int dt = 0; dt < 3; dt++)
     for (int agg = 0; agg < 2; agg++)
-      for (int sc = 0; sc < 2; sc++) {
-        e = cudaFuncSetAttribute(select_kernel(dt, agg, sc), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      for (int sc = 0; sc < 4; sc++) {
+        e = cudaFuncSetAttribute(select_kernel(dt, agg, sc & 1, sc >> 1), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute", err);
       }
   const int sms = sm_count(dev->device) * ctas;
@@ -595,7 +625,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, dev.groups,
               vec16, static_items, Dbg{dbg_skip}};
     const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * vec_bytes(dev.dtype);
-    const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr);
+    const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr, dev.coo_runs != 0);
     void *args[] = {&P, const_cast<void **>(&x), &y};
     const int threads = 32 * (1 + dev.groups * kGroupWarps);
     cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(threads), args, (size_t)smem, st);

@@ -504,3 +504,45 @@ def test_spmv_host_batch_pipelined(count, dtype):
     for yk in ring_y:
         check_rows(yk.astype(np.float64), y_ref, R, rel)
     cb.destroy(h)
+
+
+@pytest.mark.parametrize("A", CORPUS[::2], ids=lambda A: A.name)
+@pytest.mark.parametrize("dtype", ["f64", "f32", "f32f64"])
+def test_coo_run_sums_forced_on(A, dtype, monkeypatch):
+    """The aggregated kernel variant that sums same-row runs of a COO group in the warp before
+    the RED (on automatically for hub block rows), forced on for the corpus."""
+    monkeypatch.setenv("CBSPMV_COO_RUNS", "1")
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=5)
+    for agg in (0, 1):
+        y, h = gpu_spmv(A, x, dtype=dtype, agg_mode=agg)
+        if dtype == "f32":
+            y_ref, R = ref32(A, x)
+            check_rows(y, y_ref, R, 1e-5)
+        else:
+            A_ = A if dtype == "f64" else synth.CSR(A.m, A.n, A.row_ptr, A.col, A.val.astype(np.float32).astype(np.float64))
+            y_ref, R = oracle.spmv_csr(A_, x)
+            check_rows(y, y_ref, R, 1e-12)
+
+
+@pytest.mark.parametrize("pattern", ["random", "hub", "banded"])
+def test_coo_run_sums_exact_integer_bitwise(pattern, monkeypatch):
+    monkeypatch.setenv("CBSPMV_COO_RUNS", "1")
+    A = synth.random_csr(300, 260, 0.08, 17, val_mode=2, pattern=pattern)
+    x = synth.vector(A.n, synth.VEC_INT7)
+    y_ref, _ = oracle.spmv_csr(A, x)
+    for agg in (0, 1):
+        y, _ = gpu_spmv(A, x, agg_mode=agg)
+        assert np.array_equal(y, y_ref)
+
+
+def test_coo_run_sums_on_for_rmat_hubs():
+    """R-MAT has hub block rows (>= 8192 entries), so its build takes the run-summing kernel:
+    the 4096 lowest rows (the hubs) and a random sample against the oracle."""
+    _ok()
+    A = synth.make("rmat")
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=9)
+    y, h = gpu_spmv(A, x, keep_host=0)
+    rows = np.arange(4096)
+    y_ref, R = oracle.spmv_rows(A, x, rows)
+    check_rows(y[rows], y_ref, R, 1e-12)
+    sampled(A, y, x, 1e-12, k=5000, seed=4)
