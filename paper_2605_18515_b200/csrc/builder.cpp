@@ -583,7 +583,16 @@ void free_stream(Stream *s) {
 }
 
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err) {
+                 std::string *err, int64_t hub_nnz) {
+  // hub block rows (>= hub_nnz stored entries): their grouped COO blocks carry flag bit 0 in
+  // desc.row0 (a multiple of blk), telling the kernel to sum same-row runs before the RED
+  std::vector<uint8_t> hub;
+  if (hub_nnz > 0) {
+    std::vector<int64_t> brn((size_t)c.blk_m, 0);
+    for (int64_t i = 0; i < c.nb; i++) brn[(size_t)c.br[i]] += c.nnzb[i];
+    hub.assign((size_t)c.blk_m, 0);
+    for (int64_t b = 0; b < c.blk_m; b++) hub[(size_t)b] = brn[(size_t)b] >= hub_nnz;
+  }
   const int T = resolve_threads(threads);
   PhaseTimer tm;
   std::vector<int64_t> rec(c.nb);
@@ -729,6 +738,7 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
         const int64_t vals = body + round_up(idx, S);
         Desc d;
         d.row0 = (uint32_t)c.br[i] * (uint32_t)c.blk;
+        if (!hub.empty() && hub[(size_t)c.br[i]] && type == CBSPMV_FMT_COO && k <= 32) d.row0 |= 1u;
         d.xinfo = c.agg ? (uint32_t)pos : (uint32_t)c.bc[i] * (uint32_t)c.blk;
         d.offs = (uint32_t)body | ((uint32_t)vals << 16);
         d.w = pack_w((uint32_t)k, (uint32_t)type, (uint32_t)ncol[i], is_head, is_head ? gsize[i - b0] : 1u, 0u) |

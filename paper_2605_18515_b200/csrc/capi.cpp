@@ -156,23 +156,30 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   cap = (int)cb::round_up(std::max(cap, 1024), 16);
   cb::StreamPlan plan;
   const bool on_device = P->dc != nullptr;  // records on the device: fill the stream there
-  int st = cb::build_stream(c, cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err);
+  // hub block rows (power-law matrices): >= 8192 stored entries in one 16-row block row.  Their
+  // rows receive 10^4-10^5 same-address atomics per SpMV (R-MAT row 0: 115 K), serialised in L2,
+  // so their grouped COO blocks are flagged and the kernel sums same-row runs before the RED
+  // (R-MAT, 8 ranks: rank 0 0.47 -> 0.21 ms).  CBSPMV_COO_RUNS: -1 / unset = auto, 0 = off,
+  // 1 = every grouped COO block (tests).
+  int64_t hub_nnz = 8192;
+  if (const char *v = std::getenv("CBSPMV_COO_RUNS")) {
+    const int m = std::atoi(v);
+    hub_nnz = m == 0 ? 0 : (m == 1 ? 1 : hub_nnz);
+  }
+  bool has_hub = false;
+  if (hub_nnz > 0) {
+    std::vector<int64_t> brn((size_t)std::max<int64_t>(c.blk_m, 1), 0);
+    for (int64_t i = 0; i < c.nb; i++) brn[(size_t)c.br[i]] += c.nnzb[i];
+    for (int64_t v : brn) has_hub |= v >= hub_nnz;
+  }
+  int st = cb::build_stream(c, cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err,
+                            has_hub ? hub_nnz : 0);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   const int64_t npages = (int64_t)S.page_off.size() - 1;
   CbDevice &D = P->dev;
   D.device = o.device; D.dtype = dtype; D.agg = c.agg; D.m = c.m; D.n = c.n;
   D.n_pages = npages; D.page_cap = cap;
-  // hub block rows (power-law matrices): >= 8192 stored entries in one 16-row block row.  Their
-  // rows receive ~10^4-10^5 same-address atomics per SpMV, so the kernel sums same-row runs of a
-  // COO group in the warp before the RED (R-MAT, 8 ranks: rank 0 0.47 -> 0.22 ms).  Elsewhere the
-  // extra vote / scan only costs (Laplacian 0.033 -> 0.048 ms), so it is off.
-  {
-    std::vector<int64_t> brn((size_t)std::max<int64_t>(c.blk_m, 1), 0);
-    for (int64_t i = 0; i < c.nb; i++) brn[(size_t)c.br[i]] += c.nnzb[i];
-    const int64_t mx = brn.empty() ? 0 : *std::max_element(brn.begin(), brn.end());
-    D.coo_runs = mx >= 8192;
-    if (const char *v = std::getenv("CBSPMV_COO_RUNS")) D.coo_runs = std::atoi(v) != 0;
-  }
+  D.coo_runs = hub_nnz > 0 && has_hub;
   st = cb_configure(&D, err);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   // persistent CTA g streams pages [cta[g], cta[g+1]): equal byte shares

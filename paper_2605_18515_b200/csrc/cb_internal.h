@@ -124,8 +124,10 @@ struct StreamPlan {
 };
 // x_size: bytes of one x element (sizes the non-aggregated x tiles that follow each page).
 // plan == nullptr: the whole stream is written to host memory (s->bytes); otherwise only the plan.
+// hub_nnz > 0: grouped COO blocks of block rows with >= hub_nnz entries get flag bit 0 in
+// desc.row0 (the kernel sums their same-row runs before the RED).
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err);
+                 std::string *err, int64_t hub_nnz = 0);
 
 // Device-resident canonical arrays kept by the device builder for fill_stream_device.
 struct DevCanon {
@@ -199,7 +201,7 @@ struct CbDevice {
   int nstage = 0;
   int groups = 1;
   int consumers = 0;
-  int coo_runs = 0;  // hub block rows: sum same-row runs of a COO group before its RED
+  int coo_runs = 0;  // hub block rows present: the kernel variant that sums their COO runs
   const uint8_t *d_stream = nullptr;
   const uint64_t *d_page_off = nullptr;
   const uint32_t *d_cta_page = nullptr;  // grid + 1 page boundaries per persistent CTA

@@ -152,7 +152,7 @@ template <typename V>
 struct CooPend {
   V v, xv;
   uint32_t yrow;
-  bool valid;
+  bool valid, hub;  // hub: the block's row is in a hub block row (desc.row0 bit 0)
 };
 
 template <typename M, typename V, bool AGG>
@@ -172,7 +172,8 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   const M *vals = reinterpret_cast<const M *>(page + (d.z >> 16));
   const uint32_t byte = r.valid ? body[i] : 0u;
   const int col = byte >> 4;
-  r.yrow = d.x + (byte & 15);
+  r.hub = r.valid && (d.x & 1u);
+  r.yrow = (d.x & ~1u) + (byte & 15);
   r.v = r.valid ? V(vals[i]) : V(0);
   r.xv = V(0);
   if (r.valid) {
@@ -186,35 +187,37 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   return r;
 }
 
+// Runs of elements on the same y row (a COO record is sorted by (row, col)) can be
+// summed in the warp first and added by one RED from the run's first lane.  Hub rows of power-law
+// matrices otherwise receive ~10^5 same-address atomics per SpMV, serialised in L2 (R-MAT: row 0
+// gets 115 K).  Only the RUNS kernel variant does this, and only for groups holding
+// a block the builder flagged as part of a hub block row (one vote decides; then a second vote
+// skips groups without a run).
 template <typename V, bool SCALED>
 __device__ __forceinline__ void coo_finish(const CooPend<V> &r, V scale, V *__restrict__ y, Dbg dbg, bool runs) {
   V p = r.v * r.xv;
   if constexpr (SCALED) p *= scale;
-  if (runs) {
-  // Runs of elements on the same y row (a COO record is sorted by (row, col)) are
-  // summed in the warp first and added by one RED from the run's first lane.  Hub rows of
-  // power-law matrices otherwise receive ~10^5 same-address atomics per SpMV, serialised in L2
-  // (R-MAT: row 0 gets 115 K).  Groups without a run skip the scan (one vote).
-  const int lane = threadIdx.x & 31;
-  const uint32_t key = r.valid ? r.yrow : 0xFFFFFFFFu - (uint32_t)lane;  // invalid lanes: unique keys
-  const uint32_t kn = __shfl_down_sync(kFull, key, 1);
-  bool tail = lane == 31 || kn != key;  // last lane of its run
-  if (__any_sync(kFull, !tail)) {
-    const uint32_t kp = __shfl_up_sync(kFull, key, 1);
-    const bool head = lane == 0 || kp != key;
-    // segmented suffix scan: v = sum of p over [lane, end of run]
+  if (runs && __any_sync(kFull, r.hub)) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t key = r.valid ? r.yrow : 0xFFFFFFFFu - (uint32_t)lane;  // invalid lanes: unique keys
+    const uint32_t kn = __shfl_down_sync(kFull, key, 1);
+    bool tail = lane == 31 || kn != key;  // last lane of its run
+    if (__any_sync(kFull, !tail)) {
+      const uint32_t kp = __shfl_up_sync(kFull, key, 1);
+      const bool head = lane == 0 || kp != key;
+      // segmented suffix scan: p = sum over [lane, end of run]
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const V o = __shfl_down_sync(kFull, p, d);
-      const bool ot = __shfl_down_sync(kFull, tail, d);
-      if (!tail && lane + d < 32) {
-        p += o;
-        tail = ot;
+      for (int d = 1; d < 32; d <<= 1) {
+        const V o = __shfl_down_sync(kFull, p, d);
+        const bool ot = __shfl_down_sync(kFull, tail, d);
+        if (!tail && lane + d < 32) {
+          p += o;
+          tail = ot;
+        }
       }
+      if (r.valid && head) red_add(y + r.yrow, p, dbg);
+      return;
     }
-    if (r.valid && head) red_add(y + r.yrow, p, dbg);
-    return;
-  }
   }
   if (r.valid) red_add(y + r.yrow, p, dbg);
 }

@@ -236,7 +236,9 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
     for i, b in enumerate(blocks):
         br, bc = int(ex["blk_row_idx"][i]), int(ex["blk_col_idx"][i])
         nnz, typ, pg = b["nnz"], b["type"], b["page"]
-        assert b["row0"] == 16 * br and nnz == ex["nnz_per_blk"][i] and typ == ex["type_per_blk"][i]
+        # bit 0 of row0: grouped COO block of a hub block row (run sums)
+        assert b["row0"] & ~1 == 16 * br and nnz == ex["nnz_per_blk"][i] and typ == ex["type_per_blk"][i]
+        assert not b["row0"] & 1 or (typ == 0 and nnz <= 32)
         # work items: COO groups of consecutive COO blocks (nnz sum <= 32), others single
         if typ == 0 and nnz <= 32:
             assert b["lane0"] + nnz <= 32
