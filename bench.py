@@ -199,15 +199,13 @@ def run_cb(args, rank: int, world: int, local_rank: int):
     from paper_2605_18515_b200 import dist
     import synth
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+    dev, cdev = init_ranks(local_rank, world)
+    local_rank = dev.index
 
     def allreduce(a, op="sum"):
         if world == 1:
             return a
-        t = torch.from_numpy(np.asarray(a)).to(dev)
+        t = torch.from_numpy(np.asarray(a)).to(cdev)
         tdist.all_reduce(t, op=tdist.ReduceOp.SUM if op == "sum" else tdist.ReduceOp.MAX)
         return t.cpu().numpy()
 
@@ -313,6 +311,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
                 "workload": WORKLOAD[args.config], "name": args.config, "m": int(info["m"]) if world == 1 else None,
                 "nnz": int(nnz_total), "agg": int(info["agg"]), "blocks": int(info["nb"]),
                 "fmt_count_coo_csr_dense": list(info["fmt_count"]), "parallelism": f"row-shard x{world}",
+                **({"shared_gpu_test": True} if shared_gpu_test() else {}),
                 "l2": "inputs larger than L2 (matrix stream %.2f GB vs 126 MB L2); cold_l2_ms flushes 512 MB "
                       "before each step" % (info["dev_stream_bytes"] / 1e9),
                 "cold_l2_ms": cold_ms, "cold_l2_gflops": flops / (cold_ms * 1e-3) / 1e9 / world if cold_ms else None,
@@ -396,14 +395,14 @@ def run_power(args, rank, world, local_rank):
     import paper_2605_18515_b200 as cb
     from paper_2605_18515_b200 import dist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+    dev, cdev = init_ranks(local_rank, world)
+    local_rank = dev.index
+    if shared_gpu_test() and world > 1 and args.exchange != "fused":
+        raise SystemExit("CBSPMV_BENCH_SHARED_GPU runs the power iteration with --exchange fused only (gloo host collectives)")
     t0 = time.perf_counter()
     A, (r0, r1), nnz_total = make_matrix("uniform", rank, world)
     gen_s = time.perf_counter() - t0
-    agg = dist.global_agg(A, lambda a: _allreduce_np(a, dev, world), dtype=args.dtype) if world > 1 else -1
+    agg = dist.global_agg(A, lambda a: _allreduce_np(a, cdev, world), dtype=args.dtype) if world > 1 else -1
     # column panels: the auto count on one GPU (x slices L2-resident); with N ranks a multiple
     # of N so panel cuts fall on the x owners' boundaries (NEXT-1 (i) overlap)
     panels = 0 if world == 1 else world * max(1, -(-6 // world))
@@ -437,7 +436,7 @@ def run_power(args, rank, world, local_rank):
         e1.record(st)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    ms_max = float(_allreduce_np(np.array([ms]), dev, world, "max")[0])
+    ms_max = float(_allreduce_np(np.array([ms]), cdev, world, "max")[0])
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     y = torch.empty(A.m, dtype=tdt, device=dev)
     k0.record(st)
@@ -460,6 +459,7 @@ def run_power(args, rank, world, local_rank):
                        "lambda": lam, "gen_s": gen_s, "build_s": info["build_seconds"],
                        "n_panels": int(info["n_panels"]), "gather_floor": gather_floor(info, kernel_ms),
                        "exchange": args.exchange,
+                       **({"shared_gpu_test": True} if shared_gpu_test() else {}),
                        "parallelism": f"row-shard x{world}, " + {
                            "fused": "one fused finalize+exchange kernel per step over peer memory (CUDA IPC / NVLink), device flags",
                            "nccl": "NCCL all-reduce + all-gather per step",
@@ -482,6 +482,29 @@ def run_power(args, rank, world, local_rank):
     cb.destroy(h)
     if world > 1:
         tdist.destroy_process_group()
+
+
+def shared_gpu_test() -> bool:
+    """CBSPMV_BENCH_SHARED_GPU=1: a functional test of the multi-rank path on a box with fewer GPUs
+    than ranks -- ranks share GPUs (local_rank mod device count) and the host-side collectives
+    run over gloo.  Its timings are not scaling numbers (config.shared_gpu_test marks the line)."""
+    return os.environ.get("CBSPMV_BENCH_SHARED_GPU") == "1"
+
+
+def init_ranks(local_rank, world):
+    """Device of this rank and the device of its collective buffers (NCCL: the GPU; gloo: CPU)."""
+    import torch
+    import torch.distributed as tdist
+    shared = shared_gpu_test()
+    ndev = max(1, torch.cuda.device_count())
+    dev = torch.device("cuda", local_rank % ndev if shared else local_rank)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if shared:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
+    return dev, (torch.device("cpu") if shared else dev)
 
 
 def _allreduce_np(a, dev, world, op="sum"):
