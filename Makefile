@@ -48,7 +48,18 @@ $(CSRC)/exchange.o: $(CSRC)/exchange.cu $(CSRC)/cb_internal.h include/cbspmv.h
 $(LIB): $(HOST_OBJS) $(CSRC)/kernels.o $(CSRC)/gpu_builder.o $(CSRC)/exchange.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lpthread
 
+# B200 microbenchmarks behind DESIGN.md §5 (profiles/r1_microbench*.txt); not part of the library
+tools: tools/mb tools/mbg tools/mbm tools/mbga
+tools/mb: tools/microbench.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+tools/mbg: tools/mb_gather4.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $< -lcuda
+tools/mbm: tools/mb_mixed.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $< -lcuda
+tools/mbga: tools/mb_gather4_align.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $< -lcuda
+
 clean:
 	rm -f synth/libsynth.so oracle/liboracle.so $(LIB) $(CSRC)/*.o $(CSRC)/ptxas*.log
 
-.PHONY: all synth oracle lib clean
+.PHONY: all synth oracle lib tools clean
