@@ -72,3 +72,29 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     import synth
     with pytest.raises(RuntimeError):
         mod.build(synth.fig1(), device=-1)
+
+
+def test_new_entry_points_validate_arguments_without_a_gpu():
+    """cbspmv_spmv_host_batch and cbspmv_xchg_* reject bad arguments before touching CUDA."""
+    import ctypes
+
+    import numpy as np
+    import synth
+    L = cb.lib()
+    h = cb.build(synth.fig1(), device=-1)
+    xs = [np.zeros(16)]
+    ys = [np.zeros(16)]
+    xp = (ctypes.c_void_p * 1)(xs[0].ctypes.data)
+    yp = (ctypes.c_void_p * 1)(ys[0].ctypes.data)
+    assert L.cbspmv_spmv_host_batch(h.raw, xp, yp, 1, None) == 6  # host-only handle: EUNSUPPORTED
+    assert L.cbspmv_spmv_host_batch(None, xp, yp, 1, None) == 1
+    cb.destroy(h)
+    out = ctypes.c_void_p()
+    for n, dt, world, rank, dev in ((16, 0, 9, 0, 0), (16, 0, 2, 2, 0), (-1, 0, 1, 0, 0), (16, 7, 1, 0, 0),
+                                    (16, 0, 0, 0, 0), (16, 0, 1, 0, -1)):
+        assert L.cbspmv_xchg_create(n, dt, world, rank, dev, ctypes.byref(out)) == 1  # EINVAL
+        assert out.value is None
+    assert L.cbspmv_xchg_destroy(None) == 0
+    assert L.cbspmv_xchg_base(None) is None and L.cbspmv_xchg_buffer(None, 0) is None
+    assert L.cbspmv_xchg_publish(None, 0, 0, 1, 1, None) == 1
+    assert L.cbspmv_xchg_wait(None, 1, None, 1.0, None) == 1
