@@ -57,6 +57,7 @@ struct Part {
   uint8_t *d_stream = nullptr;
   uint64_t *d_page_off = nullptr;
   uint32_t *d_cta_page = nullptr;
+  uint32_t *d_page_ctr = nullptr;
   int64_t stream_bytes = 0, n_pages = 0;
   std::unique_ptr<cb::DevCanon> dc;  // device builder: records still on the device until the stream fill
 };
@@ -127,7 +128,8 @@ static void free_device(cbspmv_s *h) {
     cudaFree(p.d_stream);
     cudaFree(p.d_page_off);
     cudaFree(p.d_cta_page);
-    p.d_stream = nullptr; p.d_page_off = nullptr; p.d_cta_page = nullptr;
+    cudaFree(p.d_page_ctr);
+    p.d_stream = nullptr; p.d_page_off = nullptr; p.d_cta_page = nullptr; p.d_page_ctr = nullptr;
   }
   cudaFree(h->d_x_tmp);
   cudaFree(h->d_y_tmp);
@@ -196,6 +198,8 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   if (S.nbytes > 0) e = cudaMalloc(&P->d_stream, (size_t)S.nbytes);
   if (e == cudaSuccess) e = cudaMalloc(&P->d_page_off, S.page_off.size() * sizeof(uint64_t));
   if (e == cudaSuccess) e = cudaMalloc(&P->d_cta_page, cta.size() * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_page_ctr, cb::kCtrSlots * 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(P->d_page_ctr, 0, cb::kCtrSlots * 2 * sizeof(uint32_t), cs);
   if (e != cudaSuccess) {
     cudaGetLastError();
     cb::free_stream(&S);
@@ -228,6 +232,7 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   }
   *t_up += now() - t1;
   D.d_stream = P->d_stream; D.d_page_off = P->d_page_off; D.d_cta_page = P->d_cta_page;
+  D.d_page_ctr = P->d_page_ctr;
   P->stream_bytes = (int64_t)total;
   P->n_pages = npages;
   return CBSPMV_OK;

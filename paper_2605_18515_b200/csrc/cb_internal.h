@@ -31,6 +31,7 @@ constexpr int kPageHeader = 16;         // u32 nblk, u32 nitems, u32 item_off, u
 constexpr int kDescBytes = 16;          // see Desc
 constexpr int kDefaultStageCap = 28672;     // 8 stages in one CTA/SM; >= one fp64 TB of 8 dense blocks + tiles
 constexpr int kMaxPageCap = 65536;      // descriptor offsets are u16 bytes
+constexpr int kCtrSlots = 64;           // page-claim counters per panel (launch k uses slot k % 64)
 
 // 16-byte block descriptor, read with one 128-bit shared load.  All offsets are bytes from
 // the page start, precomputed on the host so the kernel does no record parsing.
@@ -205,6 +206,9 @@ struct CbDevice {
   const uint8_t *d_stream = nullptr;
   const uint64_t *d_page_off = nullptr;
   const uint32_t *d_cta_page = nullptr;  // grid + 1 page boundaries per persistent CTA
+  uint32_t *d_page_ctr = nullptr;         // dynamic page claiming: kCtrSlots x {next page, done}
+  mutable uint32_t ctr_next = 0;          // slot of the next launch (concurrent launches on other
+                                          // streams get their own counters)
 };
 
 // Choose grid / stages for this device; fills dev->grid, nstage, consumers.

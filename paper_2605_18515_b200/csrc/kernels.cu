@@ -37,7 +37,8 @@ constexpr int kGroupWarps = 6;     // consumer warps per group; a page is consum
 constexpr int kMaxGroups = 5;      // consumer groups per CTA (runtime: KParams::groups)
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 16;
-constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16]; warp scratch follows the ring
+constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16], end flags[16]; warp scratch follows the ring
+constexpr uint32_t kEndPage = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -311,6 +312,8 @@ struct KParams {
   const uint8_t *stream;
   const uint64_t *page_off;
   const uint32_t *cta_page;
+  uint32_t *page_ctr;  // dynamic page claiming: {next page, finished producers}; nullptr = static ranges
+  uint32_t n_pages;
   int64_t m;
   const double *sumsq;
   int stage;     // bytes per stage: page data + its x tiles
@@ -357,6 +360,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + 2 * kMaxStages;
   uint32_t *claim = reinterpret_cast<uint32_t *>(empty + kMaxStages);
+  uint32_t *stage_end = claim + kMaxStages;  // dynamic claiming: 1 = this stage ends its group's pages
   uint8_t *ring = smem + kSmemHeader;
   V *scratch = reinterpret_cast<V *>(ring + (size_t)P.nstage * P.stage);  // 16 values per consumer warp
 
@@ -381,16 +385,53 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t round = 0;
-      for (uint32_t p = p0; p < p1; p++) {
+      auto next_stage = [&]() {
         if (round > 0) {
           mbar_wait(&empty[s], (round - 1) & 1);  // every consumer warp released the stage
           claim[s] = 0;                           // published by the release of arrive below
         }
+      };
+      auto load_page = [&](uint32_t p) {
         const uint64_t off = P.page_off[p];
         const uint32_t bytes = (uint32_t)(P.page_off[p + 1] - off);
+        stage_end[s] = 0;
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(ring + (size_t)s * P.stage, P.stream + off, bytes, &full[s], pol);
         if (++s == S) { s = 0; round++; }
+      };
+      if (P.page_ctr == nullptr) {
+        for (uint32_t p = p0; p < p1; p++) {
+          next_stage();
+          load_page(p);
+        }
+      } else {
+        // Dynamic claiming (SMs that finish early take more pages): pages come from a global
+        // counter; then one end marker per consumer group (the next G stages of the sequence,
+        // so every group meets exactly one), and the last producer resets the counter for the
+        // next launch on the stream.
+        // claims of kClaim pages; the next claim is issued before the current chunk is loaded,
+        // so the atomic's round trip overlaps the stage waits and copies
+        constexpr uint32_t kClaim = 4;
+        uint32_t cur = atomicAdd(&P.page_ctr[0], kClaim);
+        while (cur < P.n_pages) {
+          const uint32_t nxt = atomicAdd(&P.page_ctr[0], kClaim);
+          const uint32_t end = min(cur + kClaim, P.n_pages);
+          for (uint32_t p = cur; p < end; p++) {
+            next_stage();
+            load_page(p);
+          }
+          cur = nxt;
+        }
+        for (int g = 0; g < P.groups; g++) {
+          next_stage();
+          stage_end[s] = 1;
+          mbar_arrive(&full[s]);  // no bytes: completes the phase, releasing the flag
+          if (++s == S) { s = 0; round++; }
+        }
+        if (atomicAdd(&P.page_ctr[1], 1u) == gridDim.x - 1) {
+          P.page_ctr[0] = 0;
+          P.page_ctr[1] = 0;
+        }
       }
     }
     return;
@@ -409,8 +450,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   constexpr bool runs = RUNS;  // hub block rows: same-row run sums before the COO REDs
   int s = grp % S;
   uint32_t parity = (uint32_t)((grp / S) & 1);
-  for (uint32_t p = p0 + grp; p < p1; p += G) {
+  const bool dyn = P.page_ctr != nullptr;
+  for (uint32_t p = p0 + grp; dyn || p < p1; p += G) {
     mbar_wait(&full[s], parity);
+    if (dyn && stage_end[s]) break;  // this group's end marker (no bytes, nothing to release)
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
     const int nitems = (dbg.skip() & 4) ? 0 : (int)hdr[1];
@@ -625,7 +668,22 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
       const char *v = std::getenv("CBSPMV_STATIC_ITEMS");  // default on (measured)
       return v ? std::atoi(v) : 1;
     }();
-    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, dev.m, sumsq, stage, dev.nstage, dev.groups,
+    // Dynamic page claiming for matrices with hub block rows (power-law: per-page work is
+    // irregular, static byte ranges leave a 9 % tail; R-MAT 1.21 -> 1.17 ms); balanced matrices
+    // keep static contiguous ranges (clustered: 0.836 vs 0.856 ms dynamic).  CBSPMV_DYNAMIC_PAGES
+    // = 0 / 1 overrides (A/B, tests).
+    static const int dynamic_env = [] {
+      const char *v = std::getenv("CBSPMV_DYNAMIC_PAGES");
+      return v ? std::atoi(v) : -1;
+    }();
+    const bool dynamic_pages = dynamic_env >= 0 ? dynamic_env != 0 : dev.coo_runs != 0;
+    uint32_t *ctr = nullptr;
+    if (dynamic_pages && dev.d_page_ctr) {
+      ctr = dev.d_page_ctr + 2 * (dev.ctr_next % cb::kCtrSlots);
+      dev.ctr_next++;
+    }
+    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.m, sumsq, stage,
+              dev.nstage, dev.groups,
               vec16, static_items, Dbg{dbg_skip}};
     const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * vec_bytes(dev.dtype);
     const void *fn = select_kernel(dev.dtype, dev.agg, sumsq != nullptr, dev.coo_runs != 0);
