@@ -668,15 +668,17 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
       const char *v = std::getenv("CBSPMV_STATIC_ITEMS");  // default on (measured)
       return v ? std::atoi(v) : 1;
     }();
-    // Dynamic page claiming for matrices with hub block rows (power-law: per-page work is
-    // irregular, static byte ranges leave a 9 % tail; R-MAT 1.21 -> 1.17 ms); balanced matrices
-    // keep static contiguous ranges (clustered: 0.836 vs 0.856 ms dynamic).  CBSPMV_DYNAMIC_PAGES
-    // = 0 / 1 overrides (A/B, tests).
+    // Dynamic page claiming for large aggregated matrices (per-page work follows the random
+    // gathers and atomics, static byte ranges leave a tail: R-MAT 1.21 -> 1.17 ms, uniform power
+    // iteration 15.5 -> 15.1 ms per step); non-aggregated matrices (clustered: 0.836 static vs
+    // 0.856 ms dynamic) and small ones (< 64 pages per CTA; Laplacian 0.034 vs 0.039 ms) keep
+    // static contiguous ranges.  CBSPMV_DYNAMIC_PAGES = 0 / 1 overrides (A/B, tests).
     static const int dynamic_env = [] {
       const char *v = std::getenv("CBSPMV_DYNAMIC_PAGES");
       return v ? std::atoi(v) : -1;
     }();
-    const bool dynamic_pages = dynamic_env >= 0 ? dynamic_env != 0 : dev.coo_runs != 0;
+    const bool dynamic_pages =
+        dynamic_env >= 0 ? dynamic_env != 0 : (dev.agg && dev.n_pages >= 64 * (int64_t)dev.grid);
     uint32_t *ctr = nullptr;
     if (dynamic_pages && dev.d_page_ctr) {
       ctr = dev.d_page_ctr + 2 * (dev.ctr_next % cb::kCtrSlots);
