@@ -671,14 +671,14 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     // Dynamic page claiming for large aggregated matrices (per-page work follows the random
     // gathers and atomics, static byte ranges leave a tail: R-MAT 1.21 -> 1.17 ms, uniform power
     // iteration 15.5 -> 15.1 ms per step); non-aggregated matrices (clustered: 0.836 static vs
-    // 0.856 ms dynamic) and small ones (< 64 pages per CTA; Laplacian 0.034 vs 0.039 ms) keep
+    // 0.856 ms dynamic) and small ones (< 32 pages per CTA; Laplacian, 20: 0.034 vs 0.039 ms) keep
     // static contiguous ranges.  CBSPMV_DYNAMIC_PAGES = 0 / 1 overrides (A/B, tests).
     static const int dynamic_env = [] {
       const char *v = std::getenv("CBSPMV_DYNAMIC_PAGES");
       return v ? std::atoi(v) : -1;
     }();
     const bool dynamic_pages =
-        dynamic_env >= 0 ? dynamic_env != 0 : (dev.agg && dev.n_pages >= 64 * (int64_t)dev.grid);
+        dynamic_env >= 0 ? dynamic_env != 0 : (dev.agg && dev.n_pages >= 32 * (int64_t)dev.grid);
     uint32_t *ctr = nullptr;
     if (dynamic_pages && dev.d_page_ctr) {
       ctr = dev.d_page_ctr + 2 * (dev.ctr_next % cb::kCtrSlots);
