@@ -284,8 +284,11 @@ def run_cb(args, rank: int, world: int, local_rank: int):
     e2e_max = float(allreduce(np.array([e2e_s]), "max")[0])
     y_dev = torch.empty(A.m, dtype=tdt, device=dev)
     cb.spmv(h, x, y_dev)
-    e2e_ok = bool(np.allclose(yhs[(args.steps - 1) % ring], y_dev.cpu().numpy(),
-                              rtol=1e-5 if args.dtype == "f32" else 1e-10, atol=0))
+    # fp atomics make the two runs differ in rounding; rows with cancellation need an absolute
+    # term scaled to the vector (the oracle-based per-row bound lives in the GPU tests)
+    yd = y_dev.cpu().numpy()
+    e2e_ok = bool(np.allclose(yhs[(args.steps - 1) % ring], yd, rtol=1e-5 if args.dtype == "f32" else 1e-10,
+                              atol=(1e-5 if args.dtype == "f32" else 1e-12) * float(np.max(np.abs(yd), initial=0.0))))
 
     flops = 2.0 * nnz_total
     value = flops / (ms_max * 1e-3) / 1e9

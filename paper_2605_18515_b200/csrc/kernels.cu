@@ -314,6 +314,7 @@ struct KParams {
   const uint32_t *cta_page;
   uint32_t *page_ctr;  // dynamic page claiming: {next page, finished producers}; nullptr = static ranges
   uint32_t n_pages;
+  uint32_t claim_chunk;  // pages per dynamic claim
   int64_t m;
   const double *sumsq;
   int stage;     // bytes per stage: page data + its x tiles
@@ -409,9 +410,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         // counter; then one end marker per consumer group (the next G stages of the sequence,
         // so every group meets exactly one), and the last producer resets the counter for the
         // next launch on the stream.
-        // claims of kClaim pages; the next claim is issued before the current chunk is loaded,
-        // so the atomic's round trip overlaps the stage waits and copies
-        constexpr uint32_t kClaim = 4;
+        // claims of claim_chunk pages (8: measured sweep at the launch site); the next claim is
+        // issued before the current chunk is loaded, so the atomic's round trip overlaps the
+        // stage waits and copies
+        const uint32_t kClaim = P.claim_chunk;
         uint32_t cur = atomicAdd(&P.page_ctr[0], kClaim);
         while (cur < P.n_pages) {
           const uint32_t nxt = atomicAdd(&P.page_ctr[0], kClaim);
@@ -684,7 +686,12 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
       ctr = dev.d_page_ctr + 2 * (dev.ctr_next % cb::kCtrSlots);
       dev.ctr_next++;
     }
-    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.m, sumsq, stage,
+    static const uint32_t claim_chunk = [] {
+      const char *v = std::getenv("CBSPMV_CLAIM_CHUNK");
+      const int c = v ? std::atoi(v) : 8;  // R-MAT: 2 -> 1.205, 4 -> 1.168, 8 -> 1.130, 32 -> 1.135 ms
+      return (uint32_t)(c < 1 ? 1 : c);
+    }();
+    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, claim_chunk, dev.m, sumsq, stage,
               dev.nstage, dev.groups,
               vec16, static_items, Dbg{dbg_skip}};
     const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * vec_bytes(dev.dtype);
