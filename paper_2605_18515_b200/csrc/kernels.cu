@@ -315,6 +315,7 @@ struct KParams {
   uint32_t *page_ctr;  // dynamic page claiming: {next page, finished producers}; nullptr = static ranges
   uint32_t n_pages;
   uint32_t claim_chunk;  // pages per dynamic claim
+  int strided;           // static: CTA g takes pages g, g + grid, ... (else a contiguous range)
   int64_t m;
   const double *sumsq;
   int stage;     // bytes per stage: page data + its x tiles
@@ -366,7 +367,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   V *scratch = reinterpret_cast<V *>(ring + (size_t)P.nstage * P.stage);  // 16 values per consumer warp
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t p0 = P.cta_page[blockIdx.x], p1 = P.cta_page[blockIdx.x + 1];
+  // static assignment: a contiguous byte-balanced page range per CTA, or (strided) pages
+  // blockIdx.x, blockIdx.x + grid, ... so every CTA sees the whole slot order's mix of formats
+  uint32_t p0 = P.cta_page[blockIdx.x], p1 = P.cta_page[blockIdx.x + 1];
+  if (P.strided) {
+    p0 = 0;
+    p1 = P.n_pages > blockIdx.x ? (P.n_pages - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;  // local count
+  }
   const int S = P.nstage;
   const Dbg dbg = P.dbg;
 
@@ -401,9 +408,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         if (++s == S) { s = 0; round++; }
       };
       if (P.page_ctr == nullptr) {
-        for (uint32_t p = p0; p < p1; p++) {
+        for (uint32_t i = p0; i < p1; i++) {
           next_stage();
-          load_page(p);
+          load_page(P.strided ? blockIdx.x + i * gridDim.x : i);
         }
       } else {
         // Dynamic claiming (SMs that finish early take more pages): pages come from a global
@@ -691,7 +698,18 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
       const int c = v ? std::atoi(v) : 8;  // R-MAT: 2 -> 1.205, 4 -> 1.168, 8 -> 1.130, 32 -> 1.135 ms
       return (uint32_t)(c < 1 ? 1 : c);
     }();
-    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, claim_chunk, dev.m, sumsq, stage,
+    // Static assignment for the rest: 4-byte stored values (fp32, mixed) are issue-bound, so
+    // each CTA takes a strided share of the slot order, mixing instruction-heavy (CSR) and light
+    // (DENSE) pages evenly (clustered fp32 0.708 -> 0.630 ms, mixed 0.781 -> 0.715 ms); fp64 is
+    // bandwidth-bound and keeps contiguous byte-balanced ranges (strided: 0.832 -> 0.856 ms).
+    // CBSPMV_STRIDED_PAGES = 0 / 1 overrides.
+    static const int strided_env = [] {
+      const char *v = std::getenv("CBSPMV_STRIDED_PAGES");
+      return v ? std::atoi(v) : -1;
+    }();
+    const int strided = ctr ? 0 : (strided_env >= 0 ? strided_env : (dev.dtype != CBSPMV_F64 ? 1 : 0));
+    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, claim_chunk, strided, dev.m,
+              sumsq, stage,
               dev.nstage, dev.groups,
               vec16, static_items, Dbg{dbg_skip}};
     const int smem = kSmemHeader + dev.nstage * stage + dev.groups * kGroupWarps * 16 * vec_bytes(dev.dtype);
