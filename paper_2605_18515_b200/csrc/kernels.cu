@@ -315,7 +315,7 @@ struct KParams {
   uint32_t *page_ctr;  // dynamic page claiming: {next page, finished producers}; nullptr = static ranges
   uint32_t n_pages;
   uint32_t claim_chunk;  // pages per dynamic claim
-  int strided;           // static: CTA g takes pages g, g + grid, ... (else a contiguous range)
+  int strided;           // static: K > 0 -> CTA g takes runs of K pages g, g + grid, ... (0: contiguous range)
   int64_t m;
   const double *sumsq;
   int stage;     // bytes per stage: page data + its x tiles
@@ -370,9 +370,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   // static assignment: a contiguous byte-balanced page range per CTA, or (strided) pages
   // blockIdx.x, blockIdx.x + grid, ... so every CTA sees the whole slot order's mix of formats
   uint32_t p0 = P.cta_page[blockIdx.x], p1 = P.cta_page[blockIdx.x + 1];
-  if (P.strided) {
+  const uint32_t K = (uint32_t)P.strided;  // strided: runs of K consecutive pages, dealt round robin
+  if (K) {
     p0 = 0;
-    p1 = P.n_pages > blockIdx.x ? (P.n_pages - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;  // local count
+    p1 = 0;  // local page count
+    for (uint64_t c = blockIdx.x; c * K < P.n_pages; c += gridDim.x) {
+      const uint64_t left = P.n_pages - c * K;
+      p1 += (uint32_t)(left < K ? left : K);
+    }
   }
   const int S = P.nstage;
   const Dbg dbg = P.dbg;
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       if (P.page_ctr == nullptr) {
         for (uint32_t i = p0; i < p1; i++) {
           next_stage();
-          load_page(P.strided ? blockIdx.x + i * gridDim.x : i);
+          load_page(K ? ((i / K) * gridDim.x + blockIdx.x) * K + i % K : i);
         }
       } else {
         // Dynamic claiming (SMs that finish early take more pages): pages come from a global
@@ -707,7 +712,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
       const char *v = std::getenv("CBSPMV_STRIDED_PAGES");
       return v ? std::atoi(v) : -1;
     }();
-    const int strided = ctr ? 0 : (strided_env >= 0 ? strided_env : (dev.dtype != CBSPMV_F64 ? 1 : 0));
+    const int strided = ctr ? 0 : (strided_env >= 0 ? strided_env : (dev.dtype != CBSPMV_F64 ? 1 : 0));  // run length
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, claim_chunk, strided, dev.m,
               sumsq, stage,
               dev.nstage, dev.groups,
