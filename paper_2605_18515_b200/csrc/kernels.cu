@@ -70,6 +70,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Consumer-side wait with a short sleep between probes (fewer issue slots and less power spent
+// spinning while the page is in flight; A/B knob CBSPMV_WAIT_SLEEP_NS, 0 = plain probe loop).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, int ns) {
+  while (!mbar_try_wait(bar, parity)) {
+    if (ns) __nanosleep(ns);
+  }
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -315,6 +322,7 @@ struct KParams {
   uint32_t *page_ctr;  // dynamic page claiming: {next page, finished producers}; nullptr = static ranges
   uint32_t n_pages;
   uint32_t claim_chunk;  // pages per dynamic claim
+  int wait_sleep_ns;     // consumers: __nanosleep between full-barrier probes
   int strided;           // static: K > 0 -> CTA g takes runs of K pages g, g + grid, ... (0: contiguous range)
   int64_t m;
   const double *sumsq;
@@ -466,7 +474,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   uint32_t parity = (uint32_t)((grp / S) & 1);
   const bool dyn = P.page_ctr != nullptr;
   for (uint32_t p = p0 + grp; dyn || p < p1; p += G) {
-    mbar_wait(&full[s], parity);
+    mbar_wait_sleep(&full[s], parity, P.wait_sleep_ns);
     if (dyn && stage_end[s]) break;  // this group's end marker (no bytes, nothing to release)
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
@@ -713,7 +721,11 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
       return v ? std::atoi(v) : -1;
     }();
     const int strided = ctr ? 0 : (strided_env >= 0 ? strided_env : (dev.dtype != CBSPMV_F64 ? 1 : 0));  // run length
-    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, claim_chunk, strided, dev.m,
+    static const int wait_sleep_ns = [] {
+      const char *v = std::getenv("CBSPMV_WAIT_SLEEP_NS");
+      return v ? std::atoi(v) : 0;
+    }();
+    KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, claim_chunk, wait_sleep_ns, strided, dev.m,
               sumsq, stage,
               dev.nstage, dev.groups,
               vec16, static_items, Dbg{dbg_skip}};
