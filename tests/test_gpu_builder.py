@@ -167,3 +167,18 @@ def test_exact_integer_bitwise_device_built(pattern):
             y = np.empty(A.m)
             cb.spmv_host(h, x, y)
             assert np.array_equal(y, y_ref)
+
+
+@pytest.mark.parametrize("A", CORPUS[::3], ids=lambda A: A.name)
+def test_device_built_with_run_sums_forced(A, monkeypatch):
+    """The hub-row flag (desc.row0 bit 0) and the run-summing kernel on device-built handles."""
+    _ok()
+    monkeypatch.setenv("CBSPMV_COO_RUNS", "1")
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=12)
+    y_ref, R = oracle.spmv_csr(A, x)
+    for agg in (0, 1):
+        h = cb.build(A, device=0, device_build=1, keep_host=0, agg_mode=agg)
+        y = np.empty(A.m)
+        cb.spmv_host(h, x, y)
+        assert np.all(np.abs(y - y_ref) <= 1e-12 * R)
+        cb.destroy(h)
