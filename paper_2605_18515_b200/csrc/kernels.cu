@@ -37,8 +37,11 @@ constexpr int kGroupWarps = 6;     // consumer warps per group; a page is consum
 constexpr int kMaxGroups = 5;      // consumer groups per CTA (runtime: KParams::groups)
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 16;
-constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16], end flags[16]; warp scratch follows the ring
+constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16]; warp scratch follows the ring
 constexpr uint32_t kEndPage = 0xFFFFFFFFu;
+// End marker of dynamic page claiming: a 16-byte page header (nblk = kEndPage) copied into the
+// stage by the same TMA path as a page, so the marker is synchronised exactly like data.
+__device__ __align__(16) const uint32_t kEndHeader[4] = {kEndPage, 0u, 16u, 16u};
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ PTX helpers
@@ -370,7 +373,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + 2 * kMaxStages;
   uint32_t *claim = reinterpret_cast<uint32_t *>(empty + kMaxStages);
-  uint32_t *stage_end = claim + kMaxStages;  // dynamic claiming: 1 = this stage ends its group's pages
   uint8_t *ring = smem + kSmemHeader;
   V *scratch = reinterpret_cast<V *>(ring + (size_t)P.nstage * P.stage);  // 16 values per consumer warp
 
@@ -415,7 +417,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       auto load_page = [&](uint32_t p) {
         const uint64_t off = P.page_off[p];
         const uint32_t bytes = (uint32_t)(P.page_off[p + 1] - off);
-        stage_end[s] = 0;
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(ring + (size_t)s * P.stage, P.stream + off, bytes, &full[s], pol);
         if (++s == S) { s = 0; round++; }
@@ -427,9 +428,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         }
       } else {
         // Dynamic claiming (SMs that finish early take more pages): pages come from a global
-        // counter; then one end marker per consumer group (the next G stages of the sequence,
-        // so every group meets exactly one), and the last producer resets the counter for the
-        // next launch on the stream.
+        // counter; then one end marker per consumer group (a 16-byte header with nblk = kEndPage
+        // in the next G stages of the sequence, so every group meets exactly one), and the last
+        // producer resets the counter for the next launch on the stream.
         // claims of claim_chunk pages (8: measured sweep at the launch site); the next claim is
         // issued before the current chunk is loaded, so the atomic's round trip overlaps the
         // stage waits and copies
@@ -446,8 +447,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         }
         for (int g = 0; g < P.groups; g++) {
           next_stage();
-          stage_end[s] = 1;
-          mbar_arrive(&full[s]);  // no bytes: completes the phase, releasing the flag
+          mbar_arrive_expect_tx(&full[s], 16u);
+          bulk_g2s(ring + (size_t)s * P.stage, kEndHeader, 16u, &full[s], pol);
           if (++s == S) { s = 0; round++; }
         }
         if (atomicAdd(&P.page_ctr[1], 1u) == gridDim.x - 1) {
@@ -475,9 +476,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   const bool dyn = P.page_ctr != nullptr;
   for (uint32_t p = p0 + grp; dyn || p < p1; p += G) {
     mbar_wait_sleep(&full[s], parity, P.wait_sleep_ns);
-    if (dyn && stage_end[s]) break;  // this group's end marker (no bytes, nothing to release)
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
+    if (dyn && hdr[0] == kEndPage) break;  // this group's end marker (nothing to release)
     const int nitems = (dbg.skip() & 4) ? 0 : (int)hdr[1];
     const uint32_t *items = reinterpret_cast<const uint32_t *>(page + hdr[2]);
     V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + hdr[3]);
