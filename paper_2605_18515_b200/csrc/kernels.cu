@@ -37,7 +37,7 @@ constexpr int kGroupWarps = 6;     // consumer warps per group; a page is consum
 constexpr int kMaxGroups = 5;      // consumer groups per CTA (runtime: KParams::groups)
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 16;
-constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16]; warp scratch follows the ring
+constexpr int kSmemHeader = 512;  // mbarriers full[16] (+16 spare), empty[16], claims[16], stage seq[16]; warp scratch follows the ring
 constexpr uint32_t kEndPage = 0xFFFFFFFFu;
 // End marker of dynamic page claiming: a 16-byte page header (nblk = kEndPage) copied into the
 // stage by the same TMA path as a page, so the marker is synchronised exactly like data.
@@ -130,6 +130,9 @@ __device__ __forceinline__ V ldg_x(const V *p, uint64_t pol) {
 // processing (bit 2) or the tile copies (bit 3).  In the production build every test folds away.
 #ifndef CBSPMV_ABLATION
 #define CBSPMV_ABLATION 0
+#endif
+#ifndef CBSPMV_CHECK  // debug build: trap on a malformed stage (pipeline race detector)
+#define CBSPMV_CHECK 0
 #endif
 struct Dbg {
   int skip_;
@@ -373,6 +376,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + 2 * kMaxStages;
   uint32_t *claim = reinterpret_cast<uint32_t *>(empty + kMaxStages);
+  // local sequence index of the page in each stage (written by the producer before its arrive)
+  volatile uint32_t *stage_seq = claim + kMaxStages;
   uint8_t *ring = smem + kSmemHeader;
   V *scratch = reinterpret_cast<V *>(ring + (size_t)P.nstage * P.stage);  // 16 values per consumer warp
 
@@ -417,6 +422,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       auto load_page = [&](uint32_t p) {
         const uint64_t off = P.page_off[p];
         const uint32_t bytes = (uint32_t)(P.page_off[p + 1] - off);
+        stage_seq[s] = round * (uint32_t)S + (uint32_t)s;
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(ring + (size_t)s * P.stage, P.stream + off, bytes, &full[s], pol);
         if (++s == S) { s = 0; round++; }
@@ -447,6 +453,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         }
         for (int g = 0; g < P.groups; g++) {
           next_stage();
+          stage_seq[s] = round * (uint32_t)S + (uint32_t)s;
           mbar_arrive_expect_tx(&full[s], 16u);
           bulk_g2s(ring + (size_t)s * P.stage, kEndHeader, 16u, &full[s], pol);
           if (++s == S) { s = 0; round++; }
@@ -474,12 +481,32 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   int s = grp % S;
   uint32_t parity = (uint32_t)((grp / S) & 1);
   const bool dyn = P.page_ctr != nullptr;
-  for (uint32_t p = p0 + grp; dyn || p < p1; p += G) {
-    mbar_wait_sleep(&full[s], parity, P.wait_sleep_ns);
+  uint32_t li = (uint32_t)grp;  // local sequence index of this group's next page
+  for (uint32_t p = p0 + grp; dyn || p < p1; p += G, li += (uint32_t)G) {
+    // Stages are shared by the groups in turn (page i -> stage i % S, group i % G), so this
+    // group can reach its round of stage s while an earlier round, another group's page, is
+    // still in flight there; the phase parity cannot tell round r + 1 from r - 1.  The producer
+    // records each page's local index in stage_seq before its arrive: wait until the stage holds
+    // ours, then wait once more (that wait can no longer alias an older phase).
+    for (;;) {
+      mbar_wait_sleep(&full[s], parity, P.wait_sleep_ns);
+      if (stage_seq[s] == li) {
+        mbar_wait(&full[s], parity);
+        break;
+      }
+      mbar_wait(&full[s], parity ^ 1u);  // the earlier round completes first
+    }
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
     if (dyn && hdr[0] == kEndPage) break;  // this group's end marker (nothing to release)
     const int nitems = (dbg.skip() & 4) ? 0 : (int)hdr[1];
+#if CBSPMV_CHECK
+    // debug build: the stage must hold a well-formed page header (a stale / torn stage traps)
+    if (hdr[2] != cb::kPageHeader + 16u * hdr[0] || hdr[0] == 0u || hdr[0] > 4096u || nitems > (int)hdr[0]) {
+      if (lane == 0) printf("bad page header cta %d warp %d s %d: %u %u %u %u\n", blockIdx.x, warp, s, hdr[0], hdr[1], hdr[2], hdr[3]);
+      __trap();
+    }
+#endif
     const uint32_t *items = reinterpret_cast<const uint32_t *>(page + hdr[2]);
     V *xbuf = reinterpret_cast<V *>(ring + (size_t)s * P.stage + hdr[3]);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
