@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kGroupWarps);
       claim[s] = 0;
+      stage_seq[s] = 0xFFFFFFFFu;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -485,17 +486,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   for (uint32_t p = p0 + grp; dyn || p < p1; p += G, li += (uint32_t)G) {
     // Stages are shared by the groups in turn (page i -> stage i % S, group i % G), so this
     // group can reach its round of stage s while an earlier round, another group's page, is
-    // still in flight there; the phase parity cannot tell round r + 1 from r - 1.  The producer
-    // records each page's local index in stage_seq before its arrive: wait until the stage holds
-    // ours, then wait once more (that wait can no longer alias an older phase).
-    for (;;) {
-      mbar_wait_sleep(&full[s], parity, P.wait_sleep_ns);
-      if (stage_seq[s] == li) {
-        mbar_wait(&full[s], parity);
-        break;
-      }
-      mbar_wait(&full[s], parity ^ 1u);  // the earlier round completes first
+    // still in flight there, and the phase parity cannot tell round r + 1 from r - 1.  The
+    // producer records each page's local index in stage_seq before its arrive, after the
+    // earlier round was released: once the stage shows our index, the parity wait is exact.
+    while (stage_seq[s] != li) {
     }
+    mbar_wait_sleep(&full[s], parity, P.wait_sleep_ns);
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
     if (dyn && hdr[0] == kEndPage) break;  // this group's end marker (nothing to release)
