@@ -489,8 +489,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     // still in flight there, and the phase parity cannot tell round r + 1 from r - 1.  The
     // producer records each page's local index in stage_seq before its arrive, after the
     // earlier round was released: once the stage shows our index, the parity wait is exact.
-    while (stage_seq[s] != li) {
-    }
+    while (stage_seq[s] != li) __nanosleep(64);  // producer not there yet: sleep, do not burn issue slots
     mbar_wait_sleep(&full[s], parity, P.wait_sleep_ns);
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t *hdr = reinterpret_cast<const uint32_t *>(page);
