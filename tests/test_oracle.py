@@ -251,6 +251,9 @@ def test_fig1_blk4_alg2():
         == g["blk4_natural_blocks"]
     cb = oracle.build(A, blk=4, th1=2, th2=8, agg_mode=0, warps_per_tb=2)
     assert cb.tb_load.tolist() == g["blk4_W2_tb_loads"]
+    # pre-LB loads (Fig. 4's sigma is reported on these): natural order, W blocks per TB
+    assert cb.tb_load_natural.tolist() == g["blk4_W2_tb_loads_natural"]
+    assert nat.tb_load_natural.tolist() == g["blk4_W2_tb_loads_natural"]
     # slot of each natural block: position within TB t is (i - tb_ptr[t])
     slot_of = {}
     for t in range(cb.T):
@@ -261,6 +264,7 @@ def test_fig1_blk4_alg2():
     assert cb.tb_ptr[1] - cb.tb_ptr[0] == 1    # TB0 has a hole (R-14)
     cb8 = oracle.build(A, blk=4, th1=2, th2=8, agg_mode=0, warps_per_tb=8)
     assert cb8.tb_load.tolist() == g["blk4_W8_tb_loads"]
+    assert cb8.tb_load_natural.tolist() == g["blk4_W8_tb_loads_natural"]
     assert unpack(cb, B=4) == entries(A)
     x = synth.vector(16, synth.VEC_FIG1)
     assert oracle.spmv_cb(cb, x).tolist() == g["y"]
