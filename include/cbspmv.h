@@ -151,7 +151,14 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
 /* y := A·x (Alg. 3 / Alg. 4 semantics).  Zeroes y, then one
  * persistent kernel streams the page stream and adds every block's products
  * into y (R-16).  x_dev: n values, y_dev: m values, double (CBSPMV_F64,
- * CBSPMV_F32F64) or float (CBSPMV_F32), aligned to their size, not aliasing. */
+ * CBSPMV_F32F64) or float (CBSPMV_F32), aligned to their size, not aliasing.
+ * Argument checks (every device-vector entry point; SURVEY §8(b) conventions): a null
+ * handle or vector, or y == x -> EINVAL; a host-only handle -> EUNSUPPORTED; a misaligned
+ * vector, a pointer that is not device (or managed) memory of the handle's device, or whose
+ * allocation ends before n (x) / m (y) values -> EDIM.  The C ABI carries no lengths: the
+ * range check is against the enclosing allocation (cuMemGetAddressRange), so a vector cut
+ * from a larger pool allocation is checked only against the pool; the Python binding checks
+ * exact lengths and dtypes.  Nothing is launched when a check fails. */
 cbspmv_status_t cbspmv_spmv(cbspmv_handle_t h, const void *x_dev, void *y_dev, void *stream);
 
 /* y += A·x (the kernel alone, no zeroing). */
@@ -190,7 +197,8 @@ cbspmv_status_t cbspmv_spmv_host_batch(cbspmv_handle_t h, const void *const *x_h
                                        int64_t count, void *stream);
 
 /* *out_dev (one double on the device) := sum_i v_i^2 over len vector values of dtype
- * (float for CBSPMV_F32, else double; the power-iteration finalize step). */
+ * (float for CBSPMV_F32, else double; the power-iteration finalize step).  v_dev and out_dev
+ * must be device memory of `device` covering len values / one double (else EDIM). */
 cbspmv_status_t cbspmv_sumsq(const void *v_dev, int64_t len, cbspmv_dtype_t dtype, double *out_dev,
                              int32_t device, void *stream);
 
@@ -287,8 +295,10 @@ cbspmv_status_t cbspmv_destroy(cbspmv_handle_t h);
  * into every peer and releases flag[r] = seq there.  No host round trip, no NCCL.
  * Ownership: the context owns its allocation and the IPC mappings it opened; destroy frees
  * them (after a device synchronise).  Errors: EINVAL (arguments, world > 8, unconnected
- * peers), ENOMEM, ECUDA.  A wait that times out (a peer never published) leaves sumsq
- * unchanged and sets the flag read by cbspmv_xchg_status. */
+ * peers), ENOMEM, ECUDA.  A wait that times out (a peer never published) poisons the
+ * context: it sets the flag read by cbspmv_xchg_status, writes sumsq = NaN (the next SpMV's
+ * iterate becomes NaN rather than a partly published one), and every later publish stores
+ * nothing and releases no flag, so every later wait times out as well. */
 #define CBSPMV_IPC_HANDLE_BYTES 64
 typedef struct cbspmv_xchg_s *cbspmv_xchg_t;
 

@@ -163,20 +163,40 @@ def default_options(**kw) -> Options:
     return o
 
 
-def _ptr(t) -> int | None:
-    """Device pointer of a torch tensor (or an int pointer) — marshalling only."""
-    if t is None:
-        return None
-    if isinstance(t, int):
+_TORCH_VEC = {np.float64: "torch.float64", np.float32: "torch.float32"}
+
+
+def _vec(t, length: int, np_dtype, device: int, what: str) -> int | None:
+    """Device pointer of a vector argument after the §8(b) checks (SURVEY §8(b) "Indexing and
+    pointers": sizes, dtype, device; the C layer re-checks device and allocation range).  A torch
+    tensor must be a contiguous CUDA tensor on the handle's device, of the handle's vector dtype,
+    with at least `length` elements; a raw integer pointer is passed through to the C checks."""
+    if t is None or isinstance(t, int):
         return t
-    if hasattr(t, "data_ptr"):
-        if not t.is_contiguous():
-            raise ValueError("tensor must be contiguous")
-        return t.data_ptr()
-    raise TypeError(type(t))
+    if not hasattr(t, "data_ptr"):
+        raise TypeError(f"{what}: expected a torch CUDA tensor or a device pointer, got {type(t).__name__}")
+    if not getattr(t, "is_cuda", False):
+        raise ValueError(f"{what}: must be a CUDA tensor (got device {t.device})")
+    if t.device.index != device:
+        raise ValueError(f"{what}: on {t.device}, the handle is on cuda:{device}")
+    if str(t.dtype) != _TORCH_VEC[np_dtype]:
+        raise TypeError(f"{what}: dtype {t.dtype}, the handle needs {_TORCH_VEC[np_dtype]}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: tensor must be contiguous")
+    if t.numel() < length:
+        raise ValueError(f"{what}: {t.numel()} elements, needs {length}")
+    return t.data_ptr()
+
+
+def _xy(h, x, y, sumsq_dev=None):
+    vt = vector_dtype(h.dtype)
+    return (_vec(x, h.info["n"], vt, h.device, "x"), _vec(y, h.info["m"], vt, h.device, "y"),
+            _vec(sumsq_dev, 1, np.float64, h.device, "sumsq"))
 
 
 def _stream(stream, device: int) -> int | None:
+    if stream is None and device < 0:  # host-only handle: the C layer refuses device calls
+        return None
     if stream is None:
         import torch
         return torch.cuda.current_stream(device).cuda_stream
@@ -256,22 +276,25 @@ def decide_agg(nb_pre: int, ss_count: int, **opts) -> int:
 
 
 def spmv(h: Handle, x, y, stream=None) -> None:
-    _check(lib().cbspmv_spmv(h.raw, _ptr(x), _ptr(y), _stream(stream, h.device)), "cbspmv_spmv")
+    xp, yp, _ = _xy(h, x, y)
+    _check(lib().cbspmv_spmv(h.raw, xp, yp, _stream(stream, h.device)), "cbspmv_spmv")
 
 
 def spmv_add(h: Handle, x, y, stream=None) -> None:
-    _check(lib().cbspmv_spmv_add(h.raw, _ptr(x), _ptr(y), _stream(stream, h.device)), "cbspmv_spmv_add")
+    xp, yp, _ = _xy(h, x, y)
+    _check(lib().cbspmv_spmv_add(h.raw, xp, yp, _stream(stream, h.device)), "cbspmv_spmv_add")
 
 
 def spmv_scaled(h: Handle, x, sumsq_dev, y, stream=None) -> None:
-    _check(lib().cbspmv_spmv_scaled(h.raw, _ptr(x), _ptr(sumsq_dev), _ptr(y), _stream(stream, h.device)),
-           "cbspmv_spmv_scaled")
+    xp, yp, sp = _xy(h, x, y, sumsq_dev)
+    _check(lib().cbspmv_spmv_scaled(h.raw, xp, sp, yp, _stream(stream, h.device)), "cbspmv_spmv_scaled")
 
 
 def spmv_panel(h: Handle, k: int, x, sumsq_dev, y, zero_y: bool, stream=None) -> None:
     """cbspmv_spmv_panel: column panel k only, y (+)= A[:, panel k] (s x); sumsq_dev None -> s = 1."""
-    _check(lib().cbspmv_spmv_panel(h.raw, int(k), _ptr(x), _ptr(sumsq_dev), _ptr(y), int(bool(zero_y)),
-                                   _stream(stream, h.device)), "cbspmv_spmv_panel")
+    xp, yp, sp = _xy(h, x, y, sumsq_dev)
+    _check(lib().cbspmv_spmv_panel(h.raw, int(k), xp, sp, yp, int(bool(zero_y)), _stream(stream, h.device)),
+           "cbspmv_spmv_panel")
 
 
 def panel_bounds(h: Handle, k: int) -> tuple[int, int]:
@@ -307,8 +330,13 @@ def spmv_host_batch(h: Handle, xs, ys, stream=None) -> None:
 
 
 def sumsq(v, out, device: int = 0, stream=None) -> None:
-    dt = F64 if str(v.dtype).endswith("float64") else F32
-    _check(lib().cbspmv_sumsq(_ptr(v), v.numel(), dt, _ptr(out), device, _stream(stream, device)), "cbspmv_sumsq")
+    """cbspmv_sumsq: out[0] := sum(v^2); v a float64 or float32 CUDA tensor, out a float64 one."""
+    if str(getattr(v, "dtype", "")) not in ("torch.float64", "torch.float32"):
+        raise TypeError(f"v: dtype {getattr(v, 'dtype', type(v).__name__)}, needs torch.float64 or torch.float32")
+    dt = F64 if str(v.dtype) == "torch.float64" else F32
+    vp = _vec(v, 0, vector_dtype(dt), device, "v")
+    op = _vec(out, 1, np.float64, device, "out")
+    _check(lib().cbspmv_sumsq(vp, v.numel(), dt, op, device, _stream(stream, device)), "cbspmv_sumsq")
 
 
 def get_info(h: Handle) -> dict:
@@ -450,7 +478,8 @@ class Exchange:
                                          _stream(stream, self.device)), "cbspmv_xchg_publish")
 
     def wait(self, seq: int, sumsq_dev, timeout_s: float = 10.0, stream=None) -> None:
-        _check(lib().cbspmv_xchg_wait(self.raw, int(seq), _ptr(sumsq_dev), float(timeout_s),
+        sp = _vec(sumsq_dev, 1, np.float64, self.device, "sumsq")
+        _check(lib().cbspmv_xchg_wait(self.raw, int(seq), sp, float(timeout_s),
                                       _stream(stream, self.device)), "cbspmv_xchg_wait")
 
     def timed_out(self) -> bool:

@@ -412,14 +412,63 @@ cbspmv_status_t cbspmv_build(int64_t m, int64_t n, int64_t nnz, const int64_t *r
   }
 }
 
-static cbspmv_status_t check_dev(cbspmv_handle_t h, const void *x, const void *y) {
+// cuMemGetAddressRange through the runtime's driver entry point (no link-time libcuda dependency,
+// so the library still loads on a machine without a driver).
+typedef int (*MemGetAddressRangeFn)(unsigned long long *base, size_t *size, unsigned long long dptr);
+static MemGetAddressRangeFn address_range_fn() {
+  static MemGetAddressRangeFn fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return (MemGetAddressRangeFn)f;
+  }();
+  return fn;
+}
+
+// A device vector argument (include/cbspmv.h "Indexing and pointers"): device memory (or managed)
+// of the handle's device, and the allocation holding it extends over `bytes` from p.  The C ABI
+// takes no lengths, so the range check is against the enclosing allocation (a caching allocator's
+// segment can be larger than the tensor; the Python binding checks exact lengths).
+static cbspmv_status_t check_vec(const void *p, size_t bytes, int device, const char *what) {
+  if (bytes == 0) return CBSPMV_OK;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CBSPMV_EDIM, std::string(what) + ": not a CUDA pointer");
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    return fail(CBSPMV_EDIM, std::string(what) + ": not device memory (host or unregistered pointer)");
+  if (a.type == cudaMemoryTypeDevice && a.device != device)
+    return fail(CBSPMV_EDIM, std::string(what) + ": on device " + std::to_string(a.device) + ", the handle is on " +
+                                 std::to_string(device));
+  if (MemGetAddressRangeFn f = address_range_fn()) {
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (f(&base, &size, (unsigned long long)(uintptr_t)p) == 0) {
+      const unsigned long long q = (unsigned long long)(uintptr_t)p;
+      if (q < base || q - base + bytes > size)
+        return fail(CBSPMV_EDIM, std::string(what) + ": the allocation ends before the vector does");
+    }
+  }
+  return CBSPMV_OK;
+}
+
+static cbspmv_status_t check_dev(cbspmv_handle_t h, const void *x, const void *y, const double *ss = nullptr) {
   if (!h) return fail(CBSPMV_EINVAL, "null handle");
   if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle (built with device = -1)");
   if ((h->info.n > 0 && !x) || (h->info.m > 0 && !y)) return fail(CBSPMV_EINVAL, "null x or y");
   const uintptr_t a = (uintptr_t)h->vec_size - 1;
   if (((uintptr_t)x & a) || ((uintptr_t)y & a)) return fail(CBSPMV_EDIM, "x / y not aligned to the value size");
   if (x && y && x == y) return fail(CBSPMV_EINVAL, "y must not alias x");
-  return CBSPMV_OK;
+  cbspmv_status_t s = check_vec(x, (size_t)h->info.n * (size_t)h->vec_size, h->device, "x");
+  if (s == CBSPMV_OK) s = check_vec(y, (size_t)h->info.m * (size_t)h->vec_size, h->device, "y");
+  if (s == CBSPMV_OK && ss) s = check_vec(ss, sizeof(double), h->device, "sumsq");
+  return s;
 }
 
 // y (+)= A·(s·x): the panels run in order, the first launch zeroes y when asked.
@@ -436,7 +485,7 @@ static int launch_all(cbspmv_handle_t h, const void *x, void *y, const double *s
 }
 
 static cbspmv_status_t run(cbspmv_handle_t h, const void *x, void *y, const double *ss, bool zero, void *stream) {
-  cbspmv_status_t s = check_dev(h, x, y);
+  cbspmv_status_t s = check_dev(h, x, y, ss);
   if (s != CBSPMV_OK) return s;
   DeviceGuard g(h->device);
   std::string err;
@@ -460,7 +509,7 @@ cbspmv_status_t cbspmv_spmv_scaled(cbspmv_handle_t h, const void *x, const doubl
 
 cbspmv_status_t cbspmv_spmv_panel(cbspmv_handle_t h, int32_t k, const void *x, const double *sumsq, void *y,
                                   int32_t zero_y, void *stream) {
-  cbspmv_status_t s = check_dev(h, x, y);
+  cbspmv_status_t s = check_dev(h, x, y, sumsq);
   if (s != CBSPMV_OK) return s;
   if (k < 0 || k >= (int32_t)h->parts.size()) return fail(CBSPMV_EINVAL, "panel index out of range");
   DeviceGuard g(h->device);
@@ -561,6 +610,9 @@ cbspmv_status_t cbspmv_sumsq(const void *v, int64_t len, cbspmv_dtype_t dtype, d
                              void *stream) {
   if (!out || (len > 0 && !v) || len < 0) return fail(CBSPMV_EINVAL, "bad sumsq arguments");
   if (!valid_dtype(dtype)) return fail(CBSPMV_EINVAL, "bad dtype");
+  cbspmv_status_t cs = check_vec(v, (size_t)len * (size_t)vec_bytes(dtype), device, "v");
+  if (cs == CBSPMV_OK) cs = check_vec(out, sizeof(double), device, "out");
+  if (cs != CBSPMV_OK) return cs;
   DeviceGuard g(device);
   std::string err;
   int st = cb_launch_sumsq(v, len, dtype, out, stream, &err);

@@ -207,8 +207,11 @@ struct CbDevice {
   const uint64_t *d_page_off = nullptr;
   const uint32_t *d_cta_page = nullptr;  // grid + 1 page boundaries per persistent CTA
   uint32_t *d_page_ctr = nullptr;         // dynamic page claiming: kCtrSlots x {next page, done}
-  mutable uint32_t ctr_next = 0;          // slot of the next launch (concurrent launches on other
-                                          // streams get their own counters)
+  mutable uint32_t ctr_next = 0;          // slot of the next launch, taken with an atomic fetch-add:
+                                          // up to kCtrSlots launches in flight (any streams, any host
+                                          // threads) get their own counters.  A captured CUDA graph
+                                          // bakes one slot into its kernel node, so replays of one
+                                          // graph must not run concurrently with each other.
 };
 
 // Choose grid / stages for this device; fills dev->grid, nstage, consumers.

@@ -66,9 +66,14 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
 }
 
 // y: this rank's slice [r0, r0 + len) of its own X[b]; stores it into every peer's X[b] at r0.
+// err: the context's timeout flag.  Once a wait has timed out the exchange is poisoned: publish
+// stores nothing into the peers (a slow peer may still be reading those buffers) and releases no
+// flag, so every later wait times out too, and the caller's status check raises.
 template <typename V>
 __global__ void __launch_bounds__(kPubThreads) xchg_publish_kernel(PubArgs A, int64_t xoff_b, int64_t r0,
-                                                                   int64_t len, Layout L, uint64_t seq) {
+                                                                   int64_t len, Layout L, uint64_t seq,
+                                                                   const int *err) {
+  if (*(const volatile int *)err) return;
   uint8_t *own = A.peer[A.rank];
   const V *y = reinterpret_cast<const V *>(own + xoff_b) + r0;
   double acc = 0.0;
@@ -108,14 +113,16 @@ __global__ void __launch_bounds__(kPubThreads) xchg_publish_kernel(PubArgs A, in
   for (int q = 0; q < A.world; q++) st_release_sys(reinterpret_cast<uint64_t *>(A.peer[q] + L.flags) + A.rank, seq);
 }
 
-// Wait until flags[q] >= seq for every rank (bounded: ~timeout_ns, then *err = 1 and no sum),
-// then sumsq = sum_q partials[(seq - 1) & 1][q] in rank order.
+// Wait until flags[q] >= seq for every rank, then sumsq = sum_q partials[(seq - 1) & 1][q] in
+// rank order.  Bounded: after ~timeout_ns (or when an earlier wait already timed out) *err = 1 and
+// sumsq = NaN, so the next SpMV's scale s = 1/sqrt(NaN) turns the iterate into NaN instead of
+// silently continuing from a partly published one.
 __global__ void xchg_wait_kernel(uint8_t *own, Layout L, int world, uint64_t seq, double *sumsq, int *err,
                                  uint64_t timeout_ns) {
   __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
+  if (threadIdx.x == 0) bad = *(volatile int *)err;
   __syncthreads();
-  if ((int)threadIdx.x < world) {
+  if (!bad && (int)threadIdx.x < world) {
     const uint64_t *f = reinterpret_cast<const uint64_t *>(own + L.flags) + threadIdx.x;
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -128,7 +135,11 @@ __global__ void xchg_wait_kernel(uint8_t *own, Layout L, int world, uint64_t seq
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  if (bad) { *err = 1; return; }
+  if (bad) {
+    *err = 1;
+    *sumsq = __longlong_as_double(0x7ff8000000000000ll);  // NaN poisons the next step
+    return;
+  }
   const int par = (int)((seq - 1) & 1);
   const volatile double *p = reinterpret_cast<const volatile double *>(own + L.partials) + par * kMaxWorld;
   double s = 0.0;
@@ -253,8 +264,8 @@ cbspmv_status_t cbspmv_xchg_publish(cbspmv_xchg_t x, int32_t b, int64_t r0, int6
   const int grid = (int)(need < 1 ? 1 : (need < x->grid ? need : x->grid));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t xoff = b ? x->L.x1 : x->L.x0;
-  if (x->vb == 8) xchg_publish_kernel<double><<<grid, kPubThreads, 0, st>>>(A, xoff, r0, len, x->L, seq);
-  else xchg_publish_kernel<float><<<grid, kPubThreads, 0, st>>>(A, xoff, r0, len, x->L, seq);
+  if (x->vb == 8) xchg_publish_kernel<double><<<grid, kPubThreads, 0, st>>>(A, xoff, r0, len, x->L, seq, x->d_err);
+  else xchg_publish_kernel<float><<<grid, kPubThreads, 0, st>>>(A, xoff, r0, len, x->L, seq, x->d_err);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_err(e, "publish launch");
   return CBSPMV_OK;

@@ -726,8 +726,9 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
         dynamic_env >= 0 ? dynamic_env != 0 : (dev.agg && dev.n_pages >= 32 * (int64_t)dev.grid);
     uint32_t *ctr = nullptr;
     if (dynamic_pages && dev.d_page_ctr) {
-      ctr = dev.d_page_ctr + 2 * (dev.ctr_next % cb::kCtrSlots);
-      dev.ctr_next++;
+      // atomic slot pick: two host threads launching the same handle get different slots
+      const uint32_t slot = __atomic_fetch_add(&dev.ctr_next, 1u, __ATOMIC_RELAXED);
+      ctr = dev.d_page_ctr + 2 * (slot % cb::kCtrSlots);
     }
     static const uint32_t claim_chunk = [] {
       const char *v = std::getenv("CBSPMV_CLAIM_CHUNK");

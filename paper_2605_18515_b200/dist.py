@@ -107,6 +107,10 @@ def power_iteration_device(h, x0, steps: int, world: int = 1, group=None, on_ste
 
     import paper_2605_18515_b200 as cb
     m_local = h.info["m"]
+    if world * m_local != x0.numel() or h.info["n"] != x0.numel():
+        # all_gather_into_tensor needs equal shards of a square matrix
+        raise ValueError(f"power_iteration_device: {world} shards of {m_local} rows do not make the "
+                         f"{x0.numel()}-long iterate (use power_iteration_overlapped / _fused for unequal shards)")
     x = x0.clone()
     y = torch.empty(m_local, dtype=x0.dtype, device=x0.device)
     ss = torch.zeros(1, dtype=torch.float64, device=x0.device)
@@ -122,6 +126,29 @@ def power_iteration_device(h, x0, steps: int, world: int = 1, group=None, on_ste
         if on_step is not None:
             on_step(k, x, ss)
     return x, ss
+
+
+def check_row_bounds(row_bounds, n: int) -> list[tuple[int, int]]:
+    """The ranks' row slices must tile [0, n) in rank order (the next x is their concatenation)."""
+    rb = [(int(a), int(b)) for a, b in row_bounds]
+    if not rb or rb[0][0] != 0 or rb[-1][1] != n or any(a > b for a, b in rb) \
+            or any(rb[i][1] != rb[i + 1][0] for i in range(len(rb) - 1)):
+        raise ValueError(f"row shards {rb} do not tile [0, {n})")
+    return rb
+
+
+def gather_row_bounds(m_local: int, n: int, world: int, group=None) -> list[tuple[int, int]]:
+    """Every rank's (r0, r1) from the shard sizes (all-gathered; shards are consecutive in rank
+    order), checked to tile [0, n).  Works for unequal shards (``equal_bounds`` with m not a
+    multiple of 16*world, or ``shard_bounds``' nnz cut)."""
+    if world == 1:
+        sizes = [int(m_local)]
+    else:
+        import torch.distributed as tdist
+        sizes = [None] * world
+        tdist.all_gather_object(sizes, int(m_local), group=group)
+    cuts = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    return check_row_bounds(list(zip(cuts[:-1], cuts[1:])), n)
 
 
 def panel_owners(c0: int, c1: int, row_bounds) -> list[int]:
@@ -198,9 +225,10 @@ def power_iteration_overlapped(h, x0, steps: int, world: int = 1, rank: int = 0,
     import torch.distributed as tdist
 
     import paper_2605_18515_b200 as cb
-    m_local = h.info["m"]
     dev = x0.device.index
-    row_bounds = [(r * m_local, (r + 1) * m_local) for r in range(world)]
+    if h.info["n"] != x0.numel():
+        raise ValueError("x0 must hold the handle's n columns")
+    row_bounds = gather_row_bounds(h.info["m"], x0.numel(), world, group)
     panels = [cb.panel_bounds(h, p) for p in range(h.info["n_panels"])]
     it = PanelPowerIteration(
         spmv_panel=lambda p, x, ss, y, z: cb.spmv_panel(h, p, x, ss, y, z),
@@ -218,7 +246,8 @@ def power_iteration_overlapped(h, x0, steps: int, world: int = 1, rank: int = 0,
 class PeerPowerIteration:
     """NEXT-1 (ii): the power-iteration exchange as one fused kernel over peer memory.
 
-    Same recurrence as ``PowerIteration``.  Every rank holds the two iterate buffers X[0], X[1].
+    Same recurrence as ``PowerIteration``.  Every rank holds the two iterate buffers X[0], X[1];
+    ``row_bounds`` (the ranks' row slices, any sizes) must tile [0, n).
     Step k: wait for flag k (every rank published step k-1; the wait also sums the ranks'
     partials of ||y_{k-1}||^2 in rank order), y_k = A_r (X[k&1] / ||.||) straight into the
     rank's own slice of X[(k+1)&1], then ``publish`` stores that slice into every peer's
@@ -230,9 +259,10 @@ class PeerPowerIteration:
     Injected ops (device: ``FusedPowerIteration``; CPU tests: numpy + gloo emulation):
     ``spmv_scaled(x, sumsq, y)``, ``publish(b, r0, length, seq)``, ``wait(seq, sumsq)``."""
 
-    def __init__(self, spmv_scaled, publish, wait, row_bounds, rank):
+    def __init__(self, spmv_scaled, publish, wait, row_bounds, rank, n=None):
         self.spmv_scaled, self.publish, self.wait = spmv_scaled, publish, wait
-        self.row_bounds = [(int(a), int(b)) for a, b in row_bounds]
+        rb = [(int(a), int(b)) for a, b in row_bounds]
+        self.row_bounds = check_row_bounds(rb, rb[-1][1] if n is None else n)
         self.rank = rank
 
     def run(self, X, sumsq, steps: int, on_step=None, k0: int = 0):
@@ -258,8 +288,11 @@ class FusedPowerIteration:
     ``cbspmv_xchg`` context per rank whose allocation every peer maps through CUDA IPC (handles
     exchanged once with ``all_gather_object``); per step one ``cbspmv_spmv_scaled`` and one
     fused ``cbspmv_xchg_publish``, the next step gated on the device by ``cbspmv_xchg_wait``.
-    Equal row shards of a square matrix.  ``run(x0, steps)`` restarts from x0 (replicated) and
-    returns (x, sumsq); x is a view of a context buffer, valid until the next run / destroy."""
+    Row shards of a square matrix, consecutive in rank order, any sizes (the bounds are
+    all-gathered and checked to tile [0, n)).  ``run(x0, steps)`` restarts from x0 (replicated)
+    and returns (x, sumsq); x is a view of a context buffer, valid until the next run / destroy.
+    A device wait that timed out (a peer never published) poisons the exchange; ``run`` checks
+    the context's status after the steps and raises."""
 
     def __init__(self, h, n: int, dtype="f64", world: int = 1, rank: int = 0, device: int = 0, group=None,
                  timeout_s: float = 30.0):
@@ -268,6 +301,9 @@ class FusedPowerIteration:
 
         import paper_2605_18515_b200 as cb
         self.h, self.world, self.rank, self.device = h, world, rank, device
+        if h.info["n"] != n:
+            raise ValueError(f"the handle has {h.info['n']} columns, the iterate {n}")
+        row_bounds = gather_row_bounds(h.info["m"], n, world, group)
         self.xc = cb.Exchange(n, dtype, world, rank, device)
         if world > 1:
             handles = [None] * world
@@ -277,13 +313,12 @@ class FusedPowerIteration:
             self.xc.connect(peer_bases=[self.xc.base()])
         self.X = [self.xc.buffer(0), self.xc.buffer(1)]
         self.ss = torch.zeros(1, dtype=torch.float64, device=f"cuda:{device}")
-        m_local = h.info["m"]
         xc = self.xc
         self.it = PeerPowerIteration(
             spmv_scaled=lambda x, s, y: cb.spmv_scaled(h, x, s, y),
             publish=lambda b, r0, ln, seq: xc.publish(b, r0, ln, seq),
             wait=lambda seq, s: xc.wait(seq, s, timeout_s),
-            row_bounds=[(r * m_local, (r + 1) * m_local) for r in range(world)], rank=rank)
+            row_bounds=row_bounds, rank=rank, n=n)
         self.k = 0
         torch.cuda.synchronize(device)
         if world > 1:
@@ -296,6 +331,9 @@ class FusedPowerIteration:
         cb.sumsq(self.X[self.k & 1], self.ss, device=self.device)
         x, ss = self.it.run(self.X, self.ss, steps, on_step=on_step, k0=self.k)
         self.k += steps
+        if self.xc.timed_out():  # synchronous status read: the run's waits have all executed
+            raise RuntimeError("fused exchange: a device wait timed out (a peer never published); "
+                               "the iterate is poisoned (NaN)")
         return x, ss
 
     def timed_out(self) -> bool:

@@ -238,14 +238,20 @@ def test_panel_power_iteration_overlap_matches_recurrence(world, P):
         assert ran == order and own_first
 
 
-def _peer_pi_worker(rank, world, port, steps, q):
+def _peer_n(world, unequal):
+    return 1000 * world + 8 if unequal else 1024 * world
+
+
+def _peer_pi_worker(rank, world, port, steps, q, unequal=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        n = 1024 * world
+        n = _peer_n(world, unequal)
         A = synth.uniform(n, n, 30, 53, val_mode=1)
-        m_loc = n // world
-        S = cbd.slice_rows(A, rank * m_loc, (rank + 1) * m_loc)
+        cuts = cbd.equal_bounds(n, world)  # unequal: n is not a multiple of 16 * world
+        S = cbd.slice_rows(A, int(cuts[rank]), int(cuts[rank + 1]))
+        row_bounds = cbd.gather_row_bounds(S.m, n, world)  # what FusedPowerIteration derives
+        assert row_bounds == [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]
         X = [torch.ones(n, dtype=torch.float64), torch.full((n,), float("nan"), dtype=torch.float64)]
         partials = np.full((2, world), np.nan)  # the context's partials[parity][rank]
         flags = [0] * world
@@ -258,9 +264,10 @@ def _peer_pi_worker(rank, world, port, steps, q):
         def publish(b, r0, length, seq):  # emulates cbspmv_xchg_publish: slice -> every peer's X[b]
             calls.append(("publish", b, seq))
             mine = X[b][r0:r0 + length].clone()
-            parts = [torch.empty_like(mine) for _ in range(world)]
-            dist.all_gather(parts, mine)
-            X[b].copy_(torch.cat(parts))
+            parts = [None] * world
+            dist.all_gather_object(parts, (r0, mine.numpy()))
+            for a, v in parts:
+                X[b][a:a + len(v)] = torch.from_numpy(v)
             tot = torch.tensor([float(torch.dot(mine, mine))], dtype=torch.float64)
             allp = [torch.empty_like(tot) for _ in range(world)]
             dist.all_gather(allp, tot)
@@ -276,8 +283,7 @@ def _peer_pi_worker(rank, world, port, steps, q):
                 s += partials[(seq - 1) & 1][r]
             ss.fill_(s)
 
-        it = cbd.PeerPowerIteration(spmv_scaled, publish, wait,
-                                    row_bounds=[(r * m_loc, (r + 1) * m_loc) for r in range(world)], rank=rank)
+        it = cbd.PeerPowerIteration(spmv_scaled, publish, wait, row_bounds=row_bounds, rank=rank, n=n)
         ss = torch.tensor([float(n)], dtype=torch.float64)
         x, ss = it.run(X, ss, steps)
         q.put((rank, float(ss.item()), x.numpy().copy(), calls))
@@ -285,22 +291,23 @@ def _peer_pi_worker(rank, world, port, steps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_power_iteration_protocol_matches_recurrence(world):
+@pytest.mark.parametrize("world,unequal", [(2, False), (3, False), (3, True)])
+def test_peer_power_iteration_protocol_matches_recurrence(world, unequal):
     """NEXT-1 (ii) host logic: wait(k) -> spmv into X[(k+1)&1] -> publish(seq k+1), double buffers
-    and partial parities, == the plain recurrence on every rank."""
+    and partial parities, == the plain recurrence on every rank.  unequal: shards of 992 / 1008 /
+    1008 rows (equal_bounds of 3008 rows), their bounds all-gathered from the shard sizes."""
     steps = 9
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_peer_pi_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_peer_pi_worker, args=(r, world, port, steps, q, unequal)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    n = 1024 * world
+    n = _peer_n(world, unequal)
     d = synth.uniform(n, n, 30, 53, val_mode=1).to_dense()
     x = np.ones(n)
     ss = float(n)
@@ -320,3 +327,15 @@ def test_peer_power_iteration_protocol_matches_recurrence(world):
         assert np.allclose(x_r, x, rtol=1e-11)
         assert [c if c[0] != "spmv" else "spmv" for c in calls] == expect
     assert len({r[1] for r in res}) == 1  # partials summed in rank order: the same bits everywhere
+
+
+def test_row_bounds_must_tile_the_iterate():
+    assert cbd.check_row_bounds([(0, 320), (320, 656), (656, 1000)], 1000) == [(0, 320), (320, 656), (656, 1000)]
+    for bad in ([(0, 320), (336, 1000)], [(0, 500)], [(16, 1000)], [(0, 600), (500, 1000)]):
+        with pytest.raises(ValueError):
+            cbd.check_row_bounds(bad, 1000)
+    assert cbd.gather_row_bounds(1000, 1000, 1) == [(0, 1000)]
+    with pytest.raises(ValueError):
+        cbd.gather_row_bounds(999, 1000, 1)
+    with pytest.raises(ValueError):  # the protocol driver refuses shards that leave a gap
+        cbd.PeerPowerIteration(None, None, None, row_bounds=[(0, 10), (12, 20)], rank=0)

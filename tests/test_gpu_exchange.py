@@ -10,6 +10,7 @@ bits.
 """
 import os
 import socket
+import time
 
 import numpy as np
 import pytest
@@ -120,15 +121,32 @@ def test_fused_exchange_f32():
 
 
 def test_fused_exchange_wait_times_out_without_publisher():
-    """A rank whose peer never publishes: the device wait gives up (bounded spin), flags it, and
-    leaves sumsq untouched -- no hang."""
+    """A rank whose peer never publishes: the device wait gives up (bounded spin), flags it and
+    poisons the context -- sumsq = NaN, later publishes store nothing into the peers and release
+    no flag, later waits fail at once -- no hang."""
     _ok()
     xcs = [cb.Exchange(64, "f64", 2, r, 0) for r in range(2)]
-    xcs[0].connect(peer_bases=[xc.base() for xc in xcs])
+    for xc in xcs:
+        xc.connect(peer_bases=[x.base() for x in xcs])
     ss = torch.full((1,), 7.0, dtype=torch.float64, device=DEV)
     xcs[0].wait(1, ss, timeout_s=0.05)
     torch.cuda.synchronize()
-    assert xcs[0].timed_out() and float(ss.item()) == 7.0
+    assert xcs[0].timed_out() and np.isnan(float(ss.item()))
+    # poisoned: rank 0's publish leaves rank 1's buffer and flags alone
+    xcs[1].buffer(1).fill_(-1.0)
+    xcs[0].buffer(1).fill_(3.0)
+    xcs[0].publish(1, 0, 32, 1)
+    ss1 = torch.zeros(1, dtype=torch.float64, device=DEV)
+    xcs[1].publish(1, 32, 32, 1)   # rank 1 is healthy: its own flag 1 is released
+    xcs[1].wait(1, ss1, timeout_s=0.05)
+    torch.cuda.synchronize()
+    assert bool((xcs[1].buffer(1)[:32] == -1.0).all())
+    assert xcs[1].timed_out()      # rank 0 never released flag 1 on rank 1
+    t0 = time.perf_counter()
+    ss.fill_(7.0)
+    xcs[0].wait(2, ss, timeout_s=5.0)  # already poisoned: returns at once, not after 5 s
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 2.0 and np.isnan(float(ss.item()))
     for xc in xcs:
         xc.destroy()
 

@@ -334,6 +334,27 @@ def test_clustered_config4_full_sampled(dtype):
         check_rows(y[rows], y_ref, R, 1e-5)
 
 
+@pytest.mark.parametrize("ff", [0, 2])
+def test_stage_round_race_regression(ff):
+    """Regression for the page-ring stage-round aliasing race: it showed with
+    forced COO / DENSE formats in natural (balance = 0) order at >= 1 M rows -- groups then run
+    out of lockstep -- as a wrong y, then illegal addresses after a few launches.  Ten
+    back-to-back launches on 2^20 rows, every one checked against the oracle on all rows."""
+    _ok()
+    A = synth.clustered(1 << 20)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=13)
+    y_ref, R = oracle.spmv_csr(A, x)
+    h = cb.build(A, device=0, force_format=ff, balance=0, agg_mode=0)
+    xd = torch.from_numpy(x).to(DEV)
+    ys = [torch.full((A.m,), float("nan"), dtype=torch.float64, device=DEV) for _ in range(10)]
+    for y in ys:
+        cb.spmv(h, xd, y)
+    torch.cuda.synchronize()
+    for y in ys:
+        check_rows(y.cpu().numpy(), y_ref, R, 1e-12)
+    cb.destroy(h)
+
+
 @pytest.mark.parametrize("name", ["clustered", "rmat"])
 def test_x_not_16_byte_aligned(name):
     """x only 8-byte aligned: the tile gather falls back from TMA bulk copies to LDGSTS."""
