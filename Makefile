@@ -31,7 +31,7 @@ synth/libsynth.so: synth/synth.c
 oracle/liboracle.so: oracle/oracle.c
 	$(CC) -O2 -fPIC -shared -Wall -Wextra -std=c11 -o $@ $<
 
-HOST_OBJS := $(CSRC)/builder.o $(CSRC)/capi.o $(CSRC)/mmio.o $(CSRC)/container.o
+HOST_OBJS := $(CSRC)/builder.o $(CSRC)/stream.o $(CSRC)/capi.o $(CSRC)/mmio.o $(CSRC)/container.o
 
 $(CSRC)/%.o: $(CSRC)/%.cpp $(CSRC)/cb_internal.h include/cbspmv.h
 	$(CXX) $(CXXFLAGS) -c -o $@ $<

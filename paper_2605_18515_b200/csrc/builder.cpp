@@ -549,228 +549,4 @@ int build_canonical(const Csr &A, const cbspmv_options_t &o, Canon *out, std::st
   return CBSPMV_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Device page stream
-// ---------------------------------------------------------------------------
-static inline int64_t dev_record_bytes(const Canon &c, int64_t i, int64_t canon_bytes, int *ncols_out) {
-  int ncols;
-  if (c.agg) {
-    int64_t w = (int64_t)(c.cols_offset[c.br[i] + 1] - c.cols_offset[c.br[i]]) - (int64_t)c.bc[i] * c.blk;
-    ncols = (int)std::min<int64_t>(c.blk, w);
-  } else {
-    ncols = (int)std::min<int64_t>(c.blk, c.n - (int64_t)c.bc[i] * c.blk);
-  }
-  *ncols_out = ncols;
-  int64_t restore_bytes = c.agg ? round_up(ncols, 4) * 4 : 0;
-  return round_up(restore_bytes + canon_bytes, 16);
-}
-
-static inline int64_t canon_record_bytes(const Canon &c, int64_t i) {
-  int64_t B = c.blk, S = c.val_size, k = c.nnzb[i];
-  int type = c.type[i];
-  int64_t idx = type == CBSPMV_FMT_COO ? k : type == CBSPMV_FMT_CSR ? (B + 1) + k : 0;
-  int64_t nval = type == CBSPMV_FMT_DENSE ? B * B : k;
-  int64_t p = idx % S;
-  return idx + (p ? S - p : 0) + nval * S;
-}
-
-void free_stream(Stream *s) {
-  if (s->bytes) {
-    if (s->pinned) cudaFreeHost(s->bytes);
-    else std::free(s->bytes);
-  }
-  s->bytes = nullptr; s->nbytes = 0; s->page_off.clear();
-}
-
-int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err, int64_t hub_nnz) {
-  // hub block rows (>= hub_nnz stored entries): their grouped COO blocks carry flag bit 0 in
-  // desc.row0 (a multiple of blk), telling the kernel to sum same-row runs before the RED
-  std::vector<uint8_t> hub;
-  if (hub_nnz > 0) {
-    std::vector<int64_t> brn((size_t)c.blk_m, 0);
-    for (int64_t i = 0; i < c.nb; i++) brn[(size_t)c.br[i]] += c.nnzb[i];
-    hub.assign((size_t)c.blk_m, 0);
-    for (int64_t b = 0; b < c.blk_m; b++) hub[(size_t)b] = brn[(size_t)b] >= hub_nnz;
-  }
-  const int T = resolve_threads(threads);
-  PhaseTimer tm;
-  std::vector<int64_t> rec(c.nb);
-  std::vector<int32_t> ncol(c.nb);
-  parallel_for(c.nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
-    for (int64_t i = lo; i < hi; i++) { int nc; rec[i] = dev_record_bytes(c, i, canon_record_bytes(c, i), &nc); ncol[i] = nc; }
-  });
-  // Work items of a block range: COO groups (<= kGroupMembers consecutive COO blocks, nnz sum
-  // <= 32) and single CSR / DENSE / large-COO blocks.  Returns the number of items.
-  auto count_items = [&](int64_t b0, int64_t b1) {
-    int64_t items = 0, lanes = 32, members = 0;
-    for (int64_t i = b0; i < b1; i++) {
-      if (c.type[i] == CBSPMV_FMT_COO && c.nnzb[i] <= 32) {
-        if (lanes + c.nnzb[i] > 32 || members == kGroupMembers) { items++; lanes = 0; members = 0; }
-        lanes += c.nnzb[i];
-        members++;
-      } else {
-        items++; lanes = 32;
-      }
-    }
-    return items;
-  };
-  auto page_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
-    return kPageHeader + kDescBytes * (b1 - b0) + round_up(4 * count_items(b0, b1), 16) + rec_bytes;
-  };
-  // x tile bytes per block gathered into the stage (non-aggregated matrices only; with aggregation
-  // the consumer lanes gather x per element)
-  const int64_t tile = c.agg ? 0 : 16 * (int64_t)x_size;
-  auto stage_bytes = [&](int64_t b0, int64_t b1, int64_t rec_bytes) {
-    return round_up(page_bytes(b0, b1, rec_bytes), 16) + tile * (b1 - b0);
-  };
-  // Greedy pages of whole thread blocks (slot order): page + x tiles <= stage capacity.
-  std::vector<int64_t> page_tb;  // first TB of each page
-  std::vector<uint64_t> off;
-  int64_t total = 0;
-  int64_t cur_tb = -1, cur_rec = 0;
-  for (int64_t t = 0; t < c.T; t++) {
-    int64_t tb_rec = 0;
-    for (int64_t i = c.tb_ptr[t]; i < c.tb_ptr[t + 1]; i++) tb_rec += rec[i];
-    if (page_cap > kMaxPageCap || stage_bytes(c.tb_ptr[t], c.tb_ptr[t + 1], tb_rec) > page_cap) {
-      *err = "stage capacity too small for one thread block";
-      return CBSPMV_EUNSUPPORTED;
-    }
-    bool fits = cur_tb >= 0 && stage_bytes(c.tb_ptr[cur_tb], c.tb_ptr[t + 1], cur_rec + tb_rec) <= page_cap;
-    if (!fits) {
-      if (cur_tb >= 0) total += round_up(page_bytes(c.tb_ptr[cur_tb], c.tb_ptr[t], cur_rec), 16);
-      page_tb.push_back(t); off.push_back((uint64_t)total);
-      cur_tb = t; cur_rec = 0;
-    }
-    cur_rec += tb_rec;
-  }
-  if (cur_tb >= 0) total += round_up(page_bytes(c.tb_ptr[cur_tb], c.tb_ptr[c.T], cur_rec), 16);
-  off.push_back((uint64_t)total);
-  page_tb.push_back(c.T);
-  const int64_t npages = (int64_t)off.size() - 1;
-
-  tm.lap("stream: page plan");
-  s->nbytes = total;
-  s->page_off = off;
-  if (plan) {  // device fill: page prefixes (header | descriptors | items) in a compact buffer
-    plan->meta_off.assign((size_t)npages + 1, 0);
-    for (int64_t p = 0; p < npages; p++) {
-      const int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
-      plan->meta_off[p + 1] = plan->meta_off[p] + (uint64_t)(kPageHeader + kDescBytes * (b1 - b0) +
-                                                             round_up(4 * count_items(b0, b1), 16));
-    }
-    plan->meta.assign((size_t)plan->meta_off[npages], 0);
-    plan->rec_dst.assign((size_t)c.nb, 0);
-    plan->res_dst.assign(c.agg ? (size_t)c.nb : 0, 0);
-    plan->ncol = ncol;
-  } else if (total > 0) {
-    void *p = nullptr;
-    // Pageable by default: pinning a multi-GB buffer costs more (measured 2.7 s for the 4.2 GB
-    // clustered stream on the B200 host) than the slower pageable copy saves.
-    static const bool want_pinned = std::getenv("CBSPMV_PINNED_STREAM") != nullptr;
-    if (want_pinned && cudaHostAlloc(&p, (size_t)total, cudaHostAllocDefault) == cudaSuccess) {
-      s->pinned = true;
-    } else {
-      if (want_pinned) cudaGetLastError();
-      p = std::malloc((size_t)total);
-      s->pinned = false;
-    }
-    if (!p) { *err = "host allocation of the page stream failed"; return CBSPMV_ENOMEM; }
-    s->bytes = (uint8_t *)p;
-  }
-  tm.lap(plan ? "stream: device plan alloc" : s->pinned ? "stream: pinned alloc" : "stream: pageable alloc");
-  parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
-    std::vector<uint32_t> w;
-    std::vector<uint16_t> items;
-    std::vector<uint32_t> iwords;
-    for (int64_t p = lo; p < hi; p++) {
-      uint8_t *page = plan ? plan->meta.data() + plan->meta_off[p] : s->bytes + off[p];
-      const int64_t b0 = c.tb_ptr[page_tb[p]], b1 = c.tb_ptr[page_tb[p + 1]];
-      const int64_t nblk = b1 - b0;
-      w.assign((size_t)nblk, 0);
-      if (!plan) std::memset(page, 0, (size_t)(off[p + 1] - off[p]));
-      // work items
-      items.clear();
-      iwords.clear();
-      int64_t lanes = 32, members = 0;
-      for (int64_t i = b0; i < b1; i++) {
-        const int64_t k = c.nnzb[i];
-        if (c.type[i] == CBSPMV_FMT_COO && k <= 32) {
-          if (lanes + k > 32 || members == kGroupMembers) {
-            items.push_back((uint16_t)(i - b0));
-            iwords.push_back(item_word((uint32_t)(i - b0), CBSPMV_FMT_COO, 1, false));
-            lanes = 0; members = 0;
-          } else {  // another member of the current group: record its first lane
-            iwords.back() += 1u << 14;
-            iwords.back() |= (uint32_t)lanes << (16 + 5 * (members - 1));
-          }
-          w[i - b0] = (uint32_t)lanes << 25;         // first lane of the block in its group
-          lanes += k;
-          members++;
-        } else {
-          items.push_back((uint16_t)(i - b0));
-          iwords.push_back(item_word((uint32_t)(i - b0), (uint32_t)c.type[i], 1, c.type[i] == CBSPMV_FMT_COO));
-          lanes = 32;
-          w[i - b0] = 0;
-        }
-      }
-      const int64_t nitems = (int64_t)items.size();
-      const int64_t item_off = kPageHeader + kDescBytes * nblk;
-      const int64_t x_off = (int64_t)(off[p + 1] - off[p]);  // x tiles follow the page in its stage
-      uint32_t hdr[4] = {(uint32_t)nblk, (uint32_t)nitems, (uint32_t)item_off, (uint32_t)x_off};
-      std::memcpy(page, hdr, 16);
-      std::memcpy(page + item_off, iwords.data(), (size_t)nitems * 4);
-      // group sizes on the heads
-      std::vector<uint32_t> gsize(nblk, 1);
-      for (int64_t it = 0; it < nitems; it++) {
-        const int64_t hb = items[it], he = it + 1 < nitems ? items[it + 1] : nblk;
-        gsize[hb] = (uint32_t)(he - hb);
-      }
-      int64_t pos = item_off + round_up(4 * nitems, 16);
-      int64_t next_item = 0;
-      for (int64_t i = b0; i < b1; i++) {
-        const int64_t k = c.nnzb[i], S = c.val_size;
-        const int type = c.type[i];
-        const bool is_head = next_item < nitems && items[next_item] == i - b0;
-        if (is_head) next_item++;
-        const int64_t idx = type == CBSPMV_FMT_COO ? k : type == CBSPMV_FMT_CSR ? (c.blk + 1) + k : 0;
-        const int64_t body = pos + (c.agg ? round_up(ncol[i], 4) * 4 : 0);
-        const int64_t vals = body + round_up(idx, S);
-        Desc d;
-        d.row0 = (uint32_t)c.br[i] * (uint32_t)c.blk;
-        if (!hub.empty() && hub[(size_t)c.br[i]] && type == CBSPMV_FMT_COO && k <= 32) d.row0 |= 1u;
-        d.xinfo = c.agg ? (uint32_t)pos : (uint32_t)c.bc[i] * (uint32_t)c.blk;
-        d.offs = (uint32_t)body | ((uint32_t)vals << 16);
-        d.w = pack_w((uint32_t)k, (uint32_t)type, (uint32_t)ncol[i], is_head, is_head ? gsize[i - b0] : 1u, 0u) |
-              w[i - b0];
-        std::memcpy(page + kPageHeader + kDescBytes * (i - b0), &d, sizeof(d));
-        if (plan) {  // records and restore entries are copied on the device (fill_stream_device)
-          plan->rec_dst[i] = off[p] + (uint64_t)body;
-          if (c.agg) plan->res_dst[i] = off[p] + (uint64_t)pos;
-          pos += rec[i];
-          continue;
-        }
-        if (c.agg) {
-          const uint32_t *seg = c.restore.data() + c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk;
-          std::memcpy(page + pos, seg, (size_t)ncol[i] * 4);
-        }
-        if (type == CBSPMV_FMT_DENSE && c.blk == 16) {
-          // lane-major device layout: slot k*32 + l holds A[l % 16][(l / 16) * 8 + k]
-          const uint8_t *src = c.mtx.data() + c.vp[i];
-          for (int k = 0; k < 8; k++)
-            for (int l = 0; l < 32; l++) {
-              const int a = (l & 15) * 16 + (l >> 4) * 8 + k;
-              std::memcpy(page + body + (int64_t)(k * 32 + l) * S, src + (int64_t)a * S, (size_t)S);
-            }
-        } else {
-          std::memcpy(page + body, c.mtx.data() + c.vp[i], (size_t)canon_record_bytes(c, i));
-        }
-        pos += rec[i];
-      }
-    }
-  });
-  tm.lap("stream: fill pages");
-  return CBSPMV_OK;
-}
-
 }  // namespace cb

@@ -153,35 +153,29 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
                        std::string *err) {
   const cb::Canon &c = P->canon;
   cb::Stream S;
-  const char *env = std::getenv("CBSPMV_PAGE_BYTES");
-  int cap = env ? std::atoi(env) : cb::kDefaultStageCap;
-  cap = (int)cb::round_up(std::max(cap, 1024), 16);
+  CbShape shape;
+  int st = cb_plan_stages(o.device, &shape, err);
+  if (st != CBSPMV_OK) return st;
   cb::StreamPlan plan;
   const bool on_device = P->dc != nullptr;  // records on the device: fill the stream there
   // hub block rows (power-law matrices): >= 8192 stored entries in one 16-row block row.  Their
   // rows receive 10^4-10^5 same-address atomics per SpMV (R-MAT row 0: 115 K), serialised in L2,
-  // so their grouped COO blocks are flagged and the kernel sums same-row runs before the RED
-  // (R-MAT, 8 ranks: rank 0 0.47 -> 0.21 ms).  CBSPMV_COO_RUNS: -1 / unset = auto, 0 = off,
-  // 1 = every grouped COO block (tests).
+  // so COO chunks with a member there are flagged and the kernel sums their same-row runs before
+  // the RED (R-MAT, 8 ranks: rank 0 0.47 -> 0.21 ms).  CBSPMV_COO_RUNS (read per build):
+  // unset = auto, 0 = off, 1 = every chunk (tests).
   int64_t hub_nnz = 8192;
   if (const char *v = std::getenv("CBSPMV_COO_RUNS")) {
     const int m = std::atoi(v);
     hub_nnz = m == 0 ? 0 : (m == 1 ? 1 : hub_nnz);
   }
-  bool has_hub = false;
-  if (hub_nnz > 0) {
-    std::vector<int64_t> brn((size_t)std::max<int64_t>(c.blk_m, 1), 0);
-    for (int64_t i = 0; i < c.nb; i++) brn[(size_t)c.br[i]] += c.nnzb[i];
-    for (int64_t v : brn) has_hub |= v >= hub_nnz;
-  }
-  int st = cb::build_stream(c, cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err,
-                            has_hub ? hub_nnz : 0);
+  st = cb::build_stream(c, shape.page_cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err,
+                        hub_nnz);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   const int64_t npages = (int64_t)S.page_off.size() - 1;
   CbDevice &D = P->dev;
+  static_cast<CbShape &>(D) = shape;
   D.device = o.device; D.dtype = dtype; D.agg = c.agg; D.m = c.m; D.n = c.n;
-  D.n_pages = npages; D.page_cap = cap;
-  D.coo_runs = hub_nnz > 0 && has_hub;
+  D.n_pages = npages;
   st = cb_configure(&D, err);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   // persistent CTA g streams pages [cta[g], cta[g+1]): equal byte shares

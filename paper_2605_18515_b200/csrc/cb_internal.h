@@ -16,47 +16,55 @@
 namespace cb {
 
 // ---------------------------------------------------------------------------
-// Device page stream.  A derived layout of the canonical
-// format: blocks in slot order (after Alg. 2), whole thread blocks per page,
-//   page = header | desc[nblk] | item[nitems] (u32 words, see item_word) | records
-// every record 16-byte aligned and preceded by its block's restore_cols entries
-// when aggregated.  One cp.async.bulk moves a whole page into a
-// shared-memory stage; the page's x tiles (16 values per block, gathered on the
-// device) follow it in the same stage, so pages are sized by
-// bytes + 16 * size(Val) * nblk <= stage capacity.  Work items: a COO group
-// (consecutive COO blocks whose nnz sum to <= 32, one warp, one lane per element)
-// or a single CSR / DENSE block.
+// Device page stream, version 2.  A derived layout of the canonical format:
+// the slot-order blocks (after Alg. 2) are cut into pages of consecutive blocks; one
+// cp.async.bulk moves a page into a shared-memory stage, and the page's x values (gathered by
+// the x warp) follow it in the same stage, so a page is sized by page bytes + x area <= stage.
+//   page = header | item descriptors (16 B each) | item records (16-B aligned)
+//   header: u32 nitems | u32 ncd (CSR / DENSE items; they come first, then the COO chunks)
+//           | u32 nblk | u32 blk0 (the page's slot-order blocks [blk0, blk0 + nblk))
+// Work items:
+//   * a CSR or DENSE block (the canonical record; DENSE values re-laid lane-major in 16-byte
+//     pairs; with aggregation its restore_cols entries precede the record);
+//   * a COO chunk: up to 32 elements of the page's COO blocks, taken in slot order (a block may
+//     continue into the next chunk), each element with its original column resolved
+//     (restore_cols[cols_offset[br] + bc*16 + c] with aggregation, bc*16 + c without) and a row
+//     byte (member << 4 | local row) indexing the chunk's table of member row bases (<= 16).
+//     chunk record = rowbase u32[nm] | rows u8[nv] (pad 4) | cols u32[nv] (pad to size(Val))
+//                    | vals[nv]; 16-byte aligned.
+// Item descriptor (uint4 a, b, c, d); d[0,2) type:
+//   CSR / DENSE: a = br*16; b = bc*16 (x tile base) or, aggregated, the page offset of the
+//                restore entries; c = record offset | values offset << 16;
+//                d[2,7) ncols (valid x-tile columns), d[8,16) nnz - 1, d[16,32) x tile offset
+//                in the stage (non-aggregated only: 16 values after the page, filled by TMA)
+//   COO chunk:   a = rowbase offset | nv << 16 | nm << 24; b = rows offset | cols offset << 16;
+//                c = values offset; d[2] hub flag (a member lies in a hub block row: the
+//                kernel sums same-row runs before the RED)
 // ---------------------------------------------------------------------------
-constexpr int kPageHeader = 16;         // u32 nblk, u32 nitems, u32 item_off, u32 x_off (x tiles in the stage)
-constexpr int kDescBytes = 16;          // see Desc
-constexpr int kDefaultStageCap = 28672;     // 8 stages in one CTA/SM; >= one fp64 TB of 8 dense blocks + tiles
-constexpr int kMaxPageCap = 65536;      // descriptor offsets are u16 bytes
-constexpr int kCtrSlots = 64;           // page-claim counters per panel (launch k uses slot k % 64)
+constexpr int kPageHeader = 16;
+constexpr int kDescBytes = 16;
+constexpr int kChunkLanes = 32;
+constexpr int kChunkMembers = 16;          // member index is 4 bits of the row byte
+constexpr uint32_t kEndItems = 0xFFFFFFFFu;  // header.nitems of the dynamic-claiming end marker
+constexpr int kMaxPageCap = 65536;         // descriptor offsets are u16 bytes
+constexpr int kCtrSlots = 64;              // page-claim counters per panel (launch k uses slot k % 64)
+constexpr uint32_t kDescHub = 1u << 2;
 
-// 16-byte block descriptor, read with one 128-bit shared load.  All offsets are bytes from
-// the page start, precomputed on the host so the kernel does no record parsing.
-struct Desc {
-  uint32_t row0;    // blk_row_idx * 16: y row base
-  uint32_t xinfo;   // without aggregation: blk_col_idx * 16 (x tile base);
-                    // with aggregation: page offset of the block's restore_cols entries
-  uint32_t offs;    // [0,16) page offset of the canonical record; [16,32) page offset of its values
-  uint32_t w;       // [0,8) nnz - 1; [8,10) type; [11,16) group size - 1 (on a group head);
-                    // [16,21) ncols (valid x-tile columns, 0..16); [24] group head;
-                    // [25,30) first lane of the block within its COO group
+#ifdef __CUDACC__
+#define CB_HD __host__ __device__
+#else
+#define CB_HD
+#endif
+struct ChunkLayout {
+  int rows, cols, vals, bytes;  // offsets from the chunk record start; total (16-aligned)
 };
-constexpr uint32_t kFlagHead = 1u << 24;
-
-// Work-item word (page item table, one u32 per item):
-//   [0,12) head block index in the page; [12,14) type; [14,16) members - 1;
-//   [16,21), [21,26), [26,31) first lane of members 1, 2, 3 of a COO group;
-//   [31] a single COO block with nnz > 32 (processed in 32-element chunks)
-constexpr int kGroupMembers = 4;
-inline uint32_t item_word(uint32_t head, uint32_t type, uint32_t members, bool big) {
-  return head | (type << 12) | ((members - 1u) << 14) | (big ? 1u << 31 : 0u);
-}
-
-inline uint32_t pack_w(uint32_t nnz, uint32_t type, uint32_t ncols, bool head, uint32_t gsize, uint32_t lane0) {
-  return (nnz - 1u) | (type << 8) | ((gsize - 1u) << 11) | (ncols << 16) | (head ? kFlagHead : 0u) | (lane0 << 25);
+CB_HD inline ChunkLayout chunk_layout(int nv, int nm, int val_size) {
+  ChunkLayout L;
+  L.rows = 4 * nm;
+  L.cols = L.rows + ((nv + 3) & ~3);
+  L.vals = (L.cols + 4 * nv + val_size - 1) / val_size * val_size;
+  L.bytes = (L.vals + val_size * nv + 15) & ~15;
+  return L;
 }
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -114,19 +122,23 @@ struct Stream {
   int64_t nbytes = 0;
   std::vector<uint64_t> page_off;  // n_pages + 1
 };
-// Device-fill plan of the page stream (device builder): the page prefixes (header | descriptors |
-// items) in a compact buffer, and per slot-order block the stream offsets of its record and restore
-// entries; the records themselves are copied on the device (fill_stream_device).
+// Device-fill plan of the page stream (device builder): the page prefixes (header | item
+// descriptors) in a compact buffer, per slot-order block the stream offset of its record (CSR /
+// DENSE) and restore entries (aggregated), per COO block its first chunk / lane / member, and per
+// chunk its record offset and shape; the records themselves are written on the device.
 struct StreamPlan {
   std::vector<uint8_t> meta;
   std::vector<uint64_t> meta_off;          // n_pages + 1
-  std::vector<uint64_t> rec_dst, res_dst;  // per block (res_dst only when aggregated)
+  std::vector<uint64_t> rec_dst, res_dst;  // per block: record / restore entries (COO: unused)
   std::vector<int32_t> ncol;               // x-tile columns per block
+  std::vector<int64_t> coo_chunk;          // per block: first chunk (COO), -1 otherwise
+  std::vector<uint8_t> coo_lane, coo_member;
+  std::vector<uint64_t> chunk_off;         // per chunk: stream offset of its record
+  std::vector<uint8_t> chunk_nv, chunk_nm;
 };
-// x_size: bytes of one x element (sizes the non-aggregated x tiles that follow each page).
+// x_size: bytes of one x element (sizes the x area that follows each page in its stage).
 // plan == nullptr: the whole stream is written to host memory (s->bytes); otherwise only the plan.
-// hub_nnz > 0: grouped COO blocks of block rows with >= hub_nnz entries get flag bit 0 in
-// desc.row0 (the kernel sums their same-row runs before the RED).
+// hub_nnz > 0: COO chunks with a member in a block row of >= hub_nnz entries get the hub flag.
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
                  std::string *err, int64_t hub_nnz = 0);
 
@@ -191,18 +203,24 @@ int resolve_threads(int t);
 // ---------------------------------------------------------------------------
 // Kernel launch interface (kernels.cu)
 // ---------------------------------------------------------------------------
-struct CbDevice {
+// Launch shape of the persistent kernel (kernels.cu cb_plan_stages): S stages of page_cap bytes,
+// G consumer groups (G divides S) of W warps, X x warps (X <= G).
+struct CbShape {
+  int nstage = 12, groups = 4, gwarps = 7, xwarps = 3, page_cap = 19008;
+};
+
+struct CbDevice : CbShape {
   int device = -1;
   int dtype = 0;
   int agg = 0;
   int64_t m = 0, n = 0;
   int64_t n_pages = 0;
-  int page_cap = 0;
   int grid = 0;
-  int nstage = 0;
-  int groups = 1;
-  int consumers = 0;
-  int coo_runs = 0;  // hub block rows present: the kernel variant that sums their COO runs
+  int sms = 0;
+  int dynamic = 0;           // dynamic page claiming (large aggregated matrices)
+  int strided = 0;           // static: runs of K pages dealt round robin (0: contiguous ranges)
+  uint32_t claim_chunk = 8;  // pages per dynamic claim
+  int dbg_skip = 0;          // ablation build only (CBSPMV_DEBUG_SKIP)
   const uint8_t *d_stream = nullptr;
   const uint64_t *d_page_off = nullptr;
   const uint32_t *d_cta_page = nullptr;  // grid + 1 page boundaries per persistent CTA
@@ -214,7 +232,10 @@ struct CbDevice {
                                           // graph must not run concurrently with each other.
 };
 
-// Choose grid / stages for this device; fills dev->grid, nstage, consumers.
+// Stage shape for a device (env CBSPMV_STAGES / CBSPMV_GROUPS / CBSPMV_GROUP_WARPS /
+// CBSPMV_PAGE_BYTES override the measured defaults; read per build).
+int cb_plan_stages(int device, CbShape *sh, std::string *err);
+// Grid and page assignment for this device and stream (dev's shape already planned).
 int cb_configure(CbDevice *dev, std::string *err);
 // y (+)= A·(s·x); zero_y: clear y first; sumsq: nullptr or device double (s = 1/sqrt(*sumsq)).
 int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *sumsq, bool zero_y,

@@ -487,8 +487,9 @@ __global__ void k_prefix(const uint8_t *__restrict__ meta, const uint64_t *__res
   }
 }
 
-// one warp per slot-order block: restore entries (aggregated) and the record; DENSE records in the
-// lane-major device layout (slot k*32 + l holds A[l % 16][(l / 16) * 8 + k])
+// one warp per slot-order CSR / DENSE block: restore entries (aggregated) and the record; DENSE
+// records re-laid in lane-major 16-byte pairs (pair q*32 + l holds A[l % 16][(l / 16) * 8 + 2q + h],
+// h = 0, 1; cb_internal.h)
 template <typename W>
 __global__ void k_records(int64_t nb, const int32_t *__restrict__ br, const int32_t *__restrict__ bc,
                           const int32_t *__restrict__ nnz, const uint8_t *__restrict__ type,
@@ -501,18 +502,63 @@ __global__ void k_records(int64_t nb, const int32_t *__restrict__ br, const int3
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (int64_t b = w0; b < nb; b += nw) {
+    const int t = type[b], k = nnz[b];
+    if (t == CBSPMV_FMT_COO) continue;  // COO blocks go into chunks (k_coo)
     if (res_dst && lane < ncol[b])
       reinterpret_cast<uint32_t *>(stream + res_dst[b])[lane] = restore[coff[br[b]] + (uint64_t)bc[b] * kBlk + lane];
-    const int t = type[b], k = nnz[b];
     const W *src = reinterpret_cast<const W *>(mtx + vp[b]);
     W *dst = reinterpret_cast<W *>(stream + rec_dst[b]);
     if (t == CBSPMV_FMT_DENSE) {
 #pragma unroll
-      for (int q = 0; q < 8; q++) dst[q * 32 + lane] = src[(lane & 15) * 16 + (lane >> 4) * 8 + q];
+      for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) dst[(q * 32 + lane) * 2 + h] = src[(lane & 15) * 16 + (lane >> 4) * 8 + 2 * q + h];
     } else {
-      const int64_t idx = t == CBSPMV_FMT_COO ? k : kBlk + 1 + k;
+      const int64_t idx = kBlk + 1 + k;
       const int64_t words = (idx + d_pad(idx, S)) / S + k;  // record bytes / S
       for (int64_t q = lane; q < words; q += 32) dst[q] = src[q];
+    }
+  }
+}
+
+// one warp per COO block: its elements into their chunks (cb_internal.h): element e sits at
+// position lane0 + e of the block's chunk run (chunk c0 + pos / 32, lane pos % 32), member m0 in the
+// first chunk and 0 in the following ones; row byte = member << 4 | local row, the column resolved
+// through restore_cols (aggregated) or bc*16 + local column.
+template <typename W>
+__global__ void k_coo(int64_t nb, const int32_t *__restrict__ br, const int32_t *__restrict__ bc,
+                      const int32_t *__restrict__ nnz, const uint64_t *__restrict__ vp,
+                      const int64_t *__restrict__ chunk, const uint8_t *__restrict__ lane0,
+                      const uint8_t *__restrict__ member0, const uint64_t *__restrict__ chunk_off,
+                      const uint8_t *__restrict__ chunk_nv, const uint8_t *__restrict__ chunk_nm,
+                      const uint8_t *__restrict__ mtx, const uint32_t *__restrict__ restore,
+                      const uint64_t *__restrict__ coff, int agg, uint8_t *__restrict__ stream) {
+  constexpr int S = (int)sizeof(W);
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = w0; b < nb; b += nw) {
+    const int64_t c0 = chunk[b];
+    if (c0 < 0) continue;
+    const int k = nnz[b], l0 = lane0[b], m0 = member0[b];
+    const uint8_t *coord = mtx + vp[b];
+    const W *vals = reinterpret_cast<const W *>(coord + k + d_pad(k, S));
+    const uint32_t row0 = (uint32_t)br[b] * kBlk;
+    const uint32_t *seg = agg ? restore + coff[br[b]] + (uint64_t)bc[b] * kBlk : nullptr;
+    const int nq = (l0 + k + 31) / 32;
+    if (lane < nq) {  // the block's row base in every chunk it touches
+      const int64_t ch = c0 + lane;
+      reinterpret_cast<uint32_t *>(stream + chunk_off[ch])[lane == 0 ? m0 : 0] = row0;
+    }
+    for (int e = lane; e < k; e += 32) {
+      const int pos = l0 + e, q = pos >> 5, l = pos & 31;
+      const int64_t ch = c0 + q;
+      const ChunkLayout L = chunk_layout(chunk_nv[ch], chunk_nm[ch], S);
+      uint8_t *r = stream + chunk_off[ch];
+      const uint32_t cb = coord[e];  // (col << 4) | row
+      r[L.rows + l] = (uint8_t)(((q ? 0 : m0) << 4) | (cb & 15));
+      reinterpret_cast<uint32_t *>(r + L.cols)[l] = seg ? seg[cb >> 4] : (uint32_t)bc[b] * kBlk + (cb >> 4);
+      reinterpret_cast<W *>(r + L.vals)[l] = vals[e];
     }
   }
 }
@@ -532,26 +578,36 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
   if (s.nbytes > 0 && !x.ok(cudaMemsetAsync(d_stream, 0, (size_t)s.nbytes, x.st), "memset stream")) return x.status;
   if (npages <= 0) return x.ok(cudaStreamSynchronize(x.st), "sync") ? CBSPMV_OK : x.status;
   DBuf d_meta, d_moff, d_poff, d_br, d_bc, d_nnz, d_type, d_vp, d_rdst, d_sdst, d_ncol;
+  DBuf d_cch, d_cl, d_cm, d_coff, d_cnv, d_cnm;
   if (!upload_vec(x, d_meta, plan.meta, "upload plan") || !upload_vec(x, d_moff, plan.meta_off, "upload plan") ||
       !upload_vec(x, d_poff, s.page_off, "upload plan") || !upload_vec(x, d_br, c.br, "upload plan") ||
       !upload_vec(x, d_bc, c.bc, "upload plan") || !upload_vec(x, d_nnz, c.nnzb, "upload plan") ||
       !upload_vec(x, d_type, c.type, "upload plan") || !upload_vec(x, d_vp, c.vp, "upload plan") ||
       !upload_vec(x, d_rdst, plan.rec_dst, "upload plan") || !upload_vec(x, d_ncol, plan.ncol, "upload plan") ||
-      (c.agg && !upload_vec(x, d_sdst, plan.res_dst, "upload plan")))
+      (c.agg && !upload_vec(x, d_sdst, plan.res_dst, "upload plan")) ||
+      !upload_vec(x, d_cch, plan.coo_chunk, "upload plan") || !upload_vec(x, d_cl, plan.coo_lane, "upload plan") ||
+      !upload_vec(x, d_cm, plan.coo_member, "upload plan") || !upload_vec(x, d_coff, plan.chunk_off, "upload plan") ||
+      !upload_vec(x, d_cnv, plan.chunk_nv, "upload plan") || !upload_vec(x, d_cnm, plan.chunk_nm, "upload plan"))
     return x.status;
   k_prefix<<<(int)std::min<int64_t>(npages, 148 * 16), 128, 0, x.st>>>(d_meta.as<uint8_t>(), d_moff.as<uint64_t>(),
                                                                       d_poff.as<uint64_t>(), npages, d_stream);
   if (nb > 0) {
     const int g = grid_for(nb * 32, 256);
     const uint64_t *rd = c.agg ? d_sdst.as<uint64_t>() : nullptr;
-    if (c.val_size == 8)
-      k_records<uint64_t><<<g, 256, 0, x.st>>>(nb, d_br.as<int32_t>(), d_bc.as<int32_t>(), d_nnz.as<int32_t>(),
-                                               d_type.as<uint8_t>(), d_vp.as<uint64_t>(), d_rdst.as<uint64_t>(), rd,
-                                               d_ncol.as<int32_t>(), dc.mtx, dc.restore, dc.cols_offset, d_stream);
-    else
-      k_records<uint32_t><<<g, 256, 0, x.st>>>(nb, d_br.as<int32_t>(), d_bc.as<int32_t>(), d_nnz.as<int32_t>(),
-                                               d_type.as<uint8_t>(), d_vp.as<uint64_t>(), d_rdst.as<uint64_t>(), rd,
-                                               d_ncol.as<int32_t>(), dc.mtx, dc.restore, dc.cols_offset, d_stream);
+#define CB_FILL(W)                                                                                                     \
+  k_records<W><<<g, 256, 0, x.st>>>(nb, d_br.as<int32_t>(), d_bc.as<int32_t>(), d_nnz.as<int32_t>(),                  \
+                                    d_type.as<uint8_t>(), d_vp.as<uint64_t>(), d_rdst.as<uint64_t>(), rd,              \
+                                    d_ncol.as<int32_t>(), dc.mtx, dc.restore, dc.cols_offset, d_stream);               \
+  k_coo<W><<<g, 256, 0, x.st>>>(nb, d_br.as<int32_t>(), d_bc.as<int32_t>(), d_nnz.as<int32_t>(), d_vp.as<uint64_t>(), \
+                                d_cch.as<int64_t>(), d_cl.as<uint8_t>(), d_cm.as<uint8_t>(), d_coff.as<uint64_t>(),   \
+                                d_cnv.as<uint8_t>(), d_cnm.as<uint8_t>(), dc.mtx, dc.restore, dc.cols_offset, c.agg,  \
+                                d_stream)
+    if (c.val_size == 8) {
+      CB_FILL(uint64_t);
+    } else {
+      CB_FILL(uint32_t);
+    }
+#undef CB_FILL
   }
   if (!x.ok(cudaGetLastError(), "fill launch") || !x.ok(cudaStreamSynchronize(x.st), "sync")) return x.status;
   return CBSPMV_OK;

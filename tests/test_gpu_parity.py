@@ -204,69 +204,118 @@ def test_dense_block_in_partial_last_block_row():
 
 # ----------------------------------------------------------------------------- device layout
 def decode_stream(stream, page_off):
-    """Decode the device page stream into per-block descriptor fields + page bytes."""
-    out = []
+    """Decode the device page stream, version 2 (cb_internal.h): per page its header,
+    item descriptors, CSR / DENSE records and COO chunk elements."""
+    pages = []
     for p in range(len(page_off) - 1):
         pg = stream[int(page_off[p]):int(page_off[p + 1])]
-        nblk = int(pg[:4].view(np.uint32)[0])
-        desc = pg[16:16 + 16 * nblk].view(np.uint32).reshape(nblk, 4)
-        for b in range(nblk):
-            row0, xinfo, offs, w = (int(v) for v in desc[b])
-            out.append(dict(row0=row0, xinfo=xinfo, body=offs & 0xFFFF, vals=offs >> 16, nnz=(w & 0xFF) + 1,
-                            type=(w >> 8) & 3, gsize=((w >> 11) & 31) + 1, ncols=(w >> 16) & 31,
-                            head=(w >> 24) & 1, lane0=(w >> 25) & 31, page=pg, slot=b, nblk=nblk))
-    return out
+        nitems, ncd, nblk, blk0 = (int(v) for v in pg[:16].view(np.uint32))
+        desc = pg[16:16 + 16 * nitems].view(np.uint32).reshape(nitems, 4)
+        items = []
+        for a, b, c, d in (tuple(int(v) for v in row) for row in desc):
+            t, xslot = d & 3, d >> 16
+            if t == 0:
+                nv, nm = (a >> 16) & 0xFF, a >> 24
+                items.append(dict(type=0, rb=a & 0xFFFF, nv=nv, nm=nm, rows=b & 0xFFFF, cols=b >> 16,
+                                  vals=c & 0xFFFF, hub=(d >> 2) & 1, xslot=xslot))
+            else:
+                items.append(dict(type=t, row0=a, xinfo=b, body=c & 0xFFFF, vals=c >> 16, ncols=(d >> 2) & 31,
+                                  nnz=((d >> 8) & 0xFF) + 1, xslot=xslot))
+        pages.append(dict(page=pg, nitems=nitems, ncd=ncd, nblk=nblk, blk0=blk0, items=items))
+    return pages
 
 
 @pytest.mark.parametrize("name", ["laplace", "rmat", "clustered"])
 @pytest.mark.parametrize("dtype", ["f64", "f32f64"])
 @pytest.mark.parametrize("device_build", [0, 1])
 def test_device_stream_encodes_canonical_format(name, dtype, device_build):
-    """What is on the device is exactly the canonical format (slot order), records byte-equal;
-    device_build=1: the stream is filled on the device from the device-built records."""
+    """What is on the device is exactly the canonical format (slot order): pages tile the slot
+    order; CSR / DENSE records byte-equal (DENSE re-laid lane-major), their restore entries equal
+    restore_cols; the COO chunks hold exactly the page's COO elements in slot order, each with its
+    original column (restore_cols resolved) and global row.  device_build=1: the stream is filled
+    on the device from the device-built records."""
     _ok()
     A = synth.make(name, small=True)
     h = cb.build(A, dtype=dtype, device=0, device_build=device_build)
     ex = cb.export(h)
     s, po = cb.download_stream(h)
-    blocks = decode_stream(s, po)
-    assert len(blocks) == ex["nb"]
+    pages = decode_stream(s, po)
     S = 8 if dtype == "f64" else 4
+    vdt = np.float64 if S == 8 else np.float32
+    xs = 8  # x / y element bytes (f64 and f32f64)
     agg = h.info["agg"]
-    for i, b in enumerate(blocks):
-        br, bc = int(ex["blk_row_idx"][i]), int(ex["blk_col_idx"][i])
-        nnz, typ, pg = b["nnz"], b["type"], b["page"]
-        # bit 0 of row0: grouped COO block of a hub block row (run sums, DESIGN.md §5)
-        assert b["row0"] & ~1 == 16 * br and nnz == ex["nnz_per_blk"][i] and typ == ex["type_per_blk"][i]
-        assert not b["row0"] & 1 or (typ == 0 and nnz <= 32)
-        # work items: COO groups of consecutive COO blocks (nnz sum <= 32), others single
-        if typ == 0 and nnz <= 32:
-            assert b["lane0"] + nnz <= 32
-            if b["head"]:
-                assert b["lane0"] == 0
+    mtx, vp = ex["mtx_data"], ex["vp_per_blk"].astype(np.int64)
+    nxt = 0
+    brn = np.bincount(ex["blk_row_idx"], weights=ex["nnz_per_blk"], minlength=1)
+    for P in pages:
+        pg = P["page"]
+        assert P["blk0"] == nxt and P["nblk"] > 0
+        blocks = range(P["blk0"], P["blk0"] + P["nblk"])
+        nxt += P["nblk"]
+        assert len(pg) % 16 == 0
+        cd = [i for i in blocks if ex["type_per_blk"][i] != 0]
+        items_cd = [it for it in P["items"] if it["type"] != 0]
+        chunks = [it for it in P["items"] if it["type"] == 0]
+        assert [it["type"] for it in P["items"]] == [1 if ex["type_per_blk"][i] == 1 else 2 for i in cd] + [0] * len(chunks)
+        assert P["ncd"] == len(cd)
+        # x tiles (non-aggregated CSR / DENSE only): 16 values each, consecutive after the page
+        end = len(pg)
+        for it in P["items"]:
+            if it["type"] and not agg:
+                assert it["xslot"] == end
+                end += 16 * xs
             else:
-                prev = blocks[i - 1]
-                assert prev["type"] == 0 and b["lane0"] == prev["lane0"] + prev["nnz"]
-        else:
-            assert b["head"] and b["gsize"] == 1 and b["lane0"] == 0
-        idx = nnz if typ == 0 else (17 + nnz if typ == 1 else 0)
-        assert b["vals"] == b["body"] + idx + (-idx) % S
-        size = idx + (-idx) % S + (256 if typ == 2 else nnz) * S
-        vp = int(ex["vp_per_blk"][i])
-        if agg:
-            seg0 = int(ex["cols_offset"][br]) + 16 * bc
-            seg1 = int(ex["cols_offset"][br + 1])
-            assert b["ncols"] == min(16, seg1 - seg0)
-            rest = pg[b["xinfo"]:b["xinfo"] + 4 * b["ncols"]].view(np.uint32)
-            assert np.array_equal(rest, ex["restore_cols"][seg0:seg0 + b["ncols"]])
-        else:
-            assert b["xinfo"] == 16 * bc and b["ncols"] == min(16, A.n - 16 * bc)
-        dev_rec = pg[b["body"]:b["body"] + size]
-        if typ == 2:  # lane-major dense layout: slot k*32 + l holds A[l % 16][(l // 16) * 8 + k]
-            k, l = np.divmod(np.arange(256), 32)
-            src = (l % 16) * 16 + (l // 16) * 8 + k
-            dev_rec = dev_rec.view(np.float64 if S == 8 else np.float32)[np.argsort(src)].view(np.uint8)
-        assert np.array_equal(dev_rec, ex["mtx_data"][vp:vp + size])
+                assert it["xslot"] == 0
+        for i, it in zip(cd, items_cd):
+            br, bc, nnz, typ = (int(ex[k][i]) for k in ("blk_row_idx", "blk_col_idx", "nnz_per_blk", "type_per_blk"))
+            assert it["row0"] == 16 * br and it["nnz"] == nnz
+            idx = 17 + nnz if typ == 1 else 0
+            assert it["vals"] == it["body"] + idx + (-idx) % S and it["body"] % 16 == 0
+            size = idx + (-idx) % S + (256 if typ == 2 else nnz) * S
+            if agg:
+                seg0 = int(ex["cols_offset"][br]) + 16 * bc
+                ncols = min(16, int(ex["cols_offset"][br + 1]) - seg0)
+                rest = pg[it["xinfo"]:it["xinfo"] + 4 * ncols].view(np.uint32)
+                assert np.array_equal(rest, ex["restore_cols"][seg0:seg0 + ncols])
+            else:
+                ncols = min(16, A.n - 16 * bc)
+                assert it["xinfo"] == 16 * bc
+            assert it["ncols"] == ncols
+            dev_rec = pg[it["body"]:it["body"] + size]
+            if typ == 2:  # lane-major pairs: value (q*32 + l)*2 + h holds A[l % 16][(l // 16) * 8 + 2q + h]
+                j = np.arange(256)
+                pair, hh = np.divmod(j, 2)
+                q, l = np.divmod(pair, 32)
+                src = (l % 16) * 16 + (l // 16) * 8 + 2 * q + hh
+                dev_rec = dev_rec.view(vdt)[np.argsort(src)].view(np.uint8)
+            assert np.array_equal(dev_rec, mtx[vp[i]:vp[i] + size])
+        # COO elements of the page in slot order: (global row, original column, value bytes)
+        want = []
+        for i in blocks:
+            if ex["type_per_blk"][i] != 0:
+                continue
+            br, bc, k = int(ex["blk_row_idx"][i]), int(ex["blk_col_idx"][i]), int(ex["nnz_per_blk"][i])
+            coord = mtx[vp[i]:vp[i] + k].astype(np.int64)
+            vals = mtx[vp[i] + k + (-k) % S:vp[i] + k + (-k) % S + k * S].view(vdt)
+            cols = (ex["restore_cols"][int(ex["cols_offset"][br]) + 16 * bc + (coord >> 4)].astype(np.int64) if agg
+                    else 16 * bc + (coord >> 4))
+            want += list(zip((16 * br + (coord & 15)).tolist(), cols.tolist(), vals.tolist()))
+        got = []
+        for it in chunks:
+            nv, nm = it["nv"], it["nm"]
+            assert 1 <= nv <= 32 and 1 <= nm <= 16 and it["rb"] % 16 == 0
+            rb = pg[it["rb"]:it["rb"] + 4 * nm].view(np.uint32).astype(np.int64)
+            assert np.all(rb % 16 == 0)
+            rows = pg[it["rows"]:it["rows"] + nv].astype(np.int64)
+            assert np.all((rows >> 4) < nm)
+            cols = pg[it["cols"]:it["cols"] + 4 * nv].view(np.uint32).astype(np.int64)
+            vals = pg[it["vals"]:it["vals"] + S * nv].view(vdt)
+            g = rb[rows >> 4] + (rows & 15)
+            if it["hub"]:
+                assert np.any(brn[g // 16] >= 8192)
+            got += list(zip(g.tolist(), cols.tolist(), vals.tolist()))
+        assert got == want
+    assert nxt == ex["nb"]
 
 
 # ----------------------------------------------------------------------------- BASELINE configs
@@ -569,3 +618,49 @@ def test_coo_run_sums_on_for_rmat_hubs():
     y_ref, R = oracle.spmv_rows(A, x, rows)
     check_rows(y[rows], y_ref, R, 1e-12)
     sampled(A, y, x, 1e-12, k=5000, seed=4)
+
+
+# ----------------------------------------------------------------------------- launch shapes / page assignment
+# Every path of the persistent kernel is chosen per handle at build time (env read by
+# cb_plan_stages / cb_configure), so each one is reachable in-process: dynamic claiming on / off,
+# strided static runs, the stage / group / warp shapes (G divides S), small pages.
+_SHAPES = [
+    {"CBSPMV_DYNAMIC_PAGES": "1"}, {"CBSPMV_DYNAMIC_PAGES": "0"},
+    {"CBSPMV_DYNAMIC_PAGES": "1", "CBSPMV_CLAIM_CHUNK": "1"},
+    {"CBSPMV_STRIDED_PAGES": "1"}, {"CBSPMV_STRIDED_PAGES": "4"}, {"CBSPMV_STRIDED_PAGES": "0"},
+    {"CBSPMV_STAGES": "8", "CBSPMV_GROUPS": "2", "CBSPMV_GROUP_WARPS": "14", "CBSPMV_XWARPS": "2"},
+    {"CBSPMV_STAGES": "12", "CBSPMV_GROUPS": "3", "CBSPMV_GROUP_WARPS": "9", "CBSPMV_XWARPS": "3"},
+    {"CBSPMV_STAGES": "4", "CBSPMV_GROUPS": "1", "CBSPMV_GROUP_WARPS": "30", "CBSPMV_XWARPS": "1"},
+    {"CBSPMV_STAGES": "30", "CBSPMV_GROUPS": "5", "CBSPMV_GROUP_WARPS": "5", "CBSPMV_XWARPS": "5"},
+    {"CBSPMV_STAGES": "16", "CBSPMV_GROUPS": "4", "CBSPMV_GROUP_WARPS": "6", "CBSPMV_XWARPS": "4"},
+    {"CBSPMV_PAGE_BYTES": "4096"},
+]
+
+
+@pytest.mark.parametrize("env", _SHAPES, ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("name", ["rmat", "clustered", "laplace"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_launch_shapes_and_page_assignment(monkeypatch, env, name, dtype):
+    _ok()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    A = synth.make(name, small=True)
+    x = synth.vector(A.n, synth.VEC_UNIFORM, seed=21)
+    y_ref, R = (oracle.spmv_csr(A, x) if dtype == "f64" else ref32(A, x))
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    h = cb.build(A, dtype=dtype, device=0)
+    xd = torch.from_numpy(x).to(DEV, tdt)
+    for _ in range(3):  # repeated launches reuse the dynamic-claim counters
+        y = torch.full((A.m,), float("nan"), dtype=tdt, device=DEV)
+        cb.spmv(h, xd, y)
+        torch.cuda.synchronize()
+        check_rows(y.cpu().numpy().astype(np.float64), y_ref, R, 1e-12 if dtype == "f64" else 1e-5)
+    cb.destroy(h)
+
+
+def test_launch_shape_rejects_too_many_warps(monkeypatch):
+    _ok()
+    monkeypatch.setenv("CBSPMV_GROUPS", "4")
+    monkeypatch.setenv("CBSPMV_GROUP_WARPS", "8")  # 1 producer + x warps + 32 consumers > 32
+    with pytest.raises(cb.CBSpMVError):
+        cb.build(synth.fig1(), device=0)
