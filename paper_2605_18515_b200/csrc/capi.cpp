@@ -158,18 +158,14 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   if (st != CBSPMV_OK) return st;
   cb::StreamPlan plan;
   const bool on_device = P->dc != nullptr;  // records on the device: fill the stream there
-  // hub block rows (power-law matrices): >= 8192 stored entries in one 16-row block row.  Their
-  // rows receive 10^4-10^5 same-address atomics per SpMV (R-MAT row 0: 115 K), serialised in L2,
-  // so COO chunks with a member there are flagged and the kernel sums their same-row runs before
-  // the RED (R-MAT, 8 ranks: rank 0 0.47 -> 0.21 ms).  CBSPMV_COO_RUNS (read per build):
-  // unset = auto, 0 = off, 1 = every chunk (tests).
-  int64_t hub_nnz = 8192;
-  if (const char *v = std::getenv("CBSPMV_COO_RUNS")) {
-    const int m = std::atoi(v);
-    hub_nnz = m == 0 ? 0 : (m == 1 ? 1 : hub_nnz);
-  }
+  // Chunks whose adjacent elements share a row get the runs flag: the kernel sums each run in the
+  // warp and issues one RED for it.  Power-law hub rows otherwise receive ~10^5 same-address
+  // atomics per SpMV, serialised in L2 (R-MAT: 1.75 -> 1.13 ms).  CBSPMV_COO_RUNS=0 (read per
+  // build) turns the flags off for A/B runs.
+  const char *rv = std::getenv("CBSPMV_COO_RUNS");
+  const bool runs = !(rv && std::atoi(rv) == 0);
   st = cb::build_stream(c, shape.page_cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err,
-                        hub_nnz);
+                        runs);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   const int64_t npages = (int64_t)S.page_off.size() - 1;
   CbDevice &D = P->dev;

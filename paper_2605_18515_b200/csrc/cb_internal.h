@@ -38,8 +38,8 @@ namespace cb {
 //                d[2,7) ncols (valid x-tile columns), d[8,16) nnz - 1, d[16,32) x tile offset
 //                in the stage (non-aggregated only: 16 values after the page, filled by TMA)
 //   COO chunk:   a = rowbase offset | nv << 16 | nm << 24; b = rows offset | cols offset << 16;
-//                c = values offset; d[2] hub flag (a member lies in a hub block row: the
-//                kernel sums same-row runs before the RED)
+//                c = values offset; d[2] runs flag (two adjacent elements share a global
+//                row: the kernel sums same-row runs in the warp before the RED)
 // ---------------------------------------------------------------------------
 constexpr int kPageHeader = 16;
 constexpr int kDescBytes = 16;
@@ -48,7 +48,7 @@ constexpr int kChunkMembers = 16;          // member index is 4 bits of the row 
 constexpr uint32_t kEndItems = 0xFFFFFFFFu;  // header.nitems of the dynamic-claiming end marker
 constexpr int kMaxPageCap = 65536;         // descriptor offsets are u16 bytes
 constexpr int kCtrSlots = 64;              // page-claim counters per panel (launch k uses slot k % 64)
-constexpr uint32_t kDescHub = 1u << 2;
+constexpr uint32_t kDescRuns = 1u << 2;
 
 #ifdef __CUDACC__
 #define CB_HD __host__ __device__
@@ -134,13 +134,15 @@ struct StreamPlan {
   std::vector<int64_t> coo_chunk;          // per block: first chunk (COO), -1 otherwise
   std::vector<uint8_t> coo_lane, coo_member;
   std::vector<uint64_t> chunk_off;         // per chunk: stream offset of its record
+  std::vector<uint64_t> chunk_desc;        // per chunk: stream offset of its descriptor
   std::vector<uint8_t> chunk_nv, chunk_nm;
+  bool runs = true;                        // set the runs flags (fill_stream_device)
 };
 // x_size: bytes of one x element (sizes the x area that follows each page in its stage).
 // plan == nullptr: the whole stream is written to host memory (s->bytes); otherwise only the plan.
-// hub_nnz > 0: COO chunks with a member in a block row of >= hub_nnz entries get the hub flag.
+// runs = false: no chunk gets the runs flag (A/B of the in-warp run sums).
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err, int64_t hub_nnz = 0);
+                 std::string *err, bool runs = true);
 
 // Device-resident canonical arrays kept by the device builder for fill_stream_device.
 struct DevCanon {

@@ -563,6 +563,28 @@ __global__ void k_coo(int64_t nb, const int32_t *__restrict__ br, const int32_t 
   }
 }
 
+// one warp per chunk: the runs flag (two adjacent elements share a global row) into its descriptor
+__global__ void k_chunk_flags(int64_t nch, const uint64_t *__restrict__ chunk_off, const uint64_t *__restrict__ chunk_desc,
+                              const uint8_t *__restrict__ chunk_nv, const uint8_t *__restrict__ chunk_nm, int S,
+                              uint8_t *__restrict__ stream) {
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t ch = w0; ch < nch; ch += nw) {
+    const int nv = chunk_nv[ch];
+    const ChunkLayout L = chunk_layout(nv, chunk_nm[ch], S);
+    const uint8_t *r = stream + chunk_off[ch];
+    uint32_t row = 0xFFFFFFFFu - (uint32_t)lane;
+    if (lane < nv) {
+      const uint32_t b = r[L.rows + lane];
+      row = reinterpret_cast<const uint32_t *>(r)[b >> 4] + (b & 15);
+    }
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, row, 1);
+    if (__any_sync(0xffffffffu, lane > 0 && lane < nv && prev == row) && lane == 0)
+      reinterpret_cast<uint32_t *>(stream + chunk_desc[ch])[3] |= kDescRuns;
+  }
+}
+
 template <class T>
 bool upload_vec(Ctx &x, DBuf &d, const std::vector<T> &v, const char *what) {
   return x.alloc(d, sizeof(T) * v.size(), what) &&
@@ -578,7 +600,7 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
   if (s.nbytes > 0 && !x.ok(cudaMemsetAsync(d_stream, 0, (size_t)s.nbytes, x.st), "memset stream")) return x.status;
   if (npages <= 0) return x.ok(cudaStreamSynchronize(x.st), "sync") ? CBSPMV_OK : x.status;
   DBuf d_meta, d_moff, d_poff, d_br, d_bc, d_nnz, d_type, d_vp, d_rdst, d_sdst, d_ncol;
-  DBuf d_cch, d_cl, d_cm, d_coff, d_cnv, d_cnm;
+  DBuf d_cch, d_cl, d_cm, d_coff, d_cnv, d_cnm, d_cdesc;
   if (!upload_vec(x, d_meta, plan.meta, "upload plan") || !upload_vec(x, d_moff, plan.meta_off, "upload plan") ||
       !upload_vec(x, d_poff, s.page_off, "upload plan") || !upload_vec(x, d_br, c.br, "upload plan") ||
       !upload_vec(x, d_bc, c.bc, "upload plan") || !upload_vec(x, d_nnz, c.nnzb, "upload plan") ||
@@ -587,7 +609,8 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
       (c.agg && !upload_vec(x, d_sdst, plan.res_dst, "upload plan")) ||
       !upload_vec(x, d_cch, plan.coo_chunk, "upload plan") || !upload_vec(x, d_cl, plan.coo_lane, "upload plan") ||
       !upload_vec(x, d_cm, plan.coo_member, "upload plan") || !upload_vec(x, d_coff, plan.chunk_off, "upload plan") ||
-      !upload_vec(x, d_cnv, plan.chunk_nv, "upload plan") || !upload_vec(x, d_cnm, plan.chunk_nm, "upload plan"))
+      !upload_vec(x, d_cnv, plan.chunk_nv, "upload plan") || !upload_vec(x, d_cnm, plan.chunk_nm, "upload plan") ||
+      !upload_vec(x, d_cdesc, plan.chunk_desc, "upload plan"))
     return x.status;
   k_prefix<<<(int)std::min<int64_t>(npages, 148 * 16), 128, 0, x.st>>>(d_meta.as<uint8_t>(), d_moff.as<uint64_t>(),
                                                                       d_poff.as<uint64_t>(), npages, d_stream);
@@ -608,6 +631,11 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
       CB_FILL(uint32_t);
     }
 #undef CB_FILL
+    const int64_t nch = (int64_t)plan.chunk_off.size();
+    if (plan.runs && nch > 0)
+      k_chunk_flags<<<grid_for(nch * 32, 256), 256, 0, x.st>>>(nch, d_coff.as<uint64_t>(), d_cdesc.as<uint64_t>(),
+                                                             d_cnv.as<uint8_t>(), d_cnm.as<uint8_t>(), c.val_size,
+                                                             d_stream);
   }
   if (!x.ok(cudaGetLastError(), "fill launch") || !x.ok(cudaStreamSynchronize(x.st), "sync")) return x.status;
   return CBSPMV_OK;

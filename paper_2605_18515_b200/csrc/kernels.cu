@@ -16,8 +16,8 @@
 //       atomicAdd:
 //       * COO chunk (Alg. 3): lane <-> element, x[col] gathered into a register
 //         (four chunks' loads in flight per warp); one RED per element issued as one warp
-//         instruction for up to 32 elements; chunks with hub-row members sum same-row runs in
-//         the warp first (one RED per run);
+//         instruction for up to 32 elements; chunks with same-row runs sum them in the warp
+//         first (one RED per run);
 //       * CSR ("32 threads collaboratively compute 16 y elements"): two lanes per
 //         row, one shfl_xor; x tile from the stage (aggregated: gathered through the restore
 //         entries into the warp's scratch);
@@ -137,7 +137,7 @@ template <typename V>
 struct CooPend {
   V v, xv;
   uint32_t row;
-  bool valid, hub;
+  bool valid, runs;
 };
 
 template <typename M, typename V>
@@ -146,7 +146,7 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   CooPend<V> r;
   const int nv = (d.x >> 16) & 0xFF;
   r.valid = lane < nv;
-  r.hub = (d.w & cb::kDescHub) != 0;
+  r.runs = (d.w & cb::kDescRuns) != 0;
   const uint8_t *rows = page + (d.y & 0xFFFFu);
   const uint32_t *cols = reinterpret_cast<const uint32_t *>(page + (d.y >> 16));
   const M *vals = reinterpret_cast<const M *>(page + (d.z & 0xFFFFu));
@@ -159,19 +159,19 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   return r;
 }
 
-// Hub chunks (desc bit 2: a member in a block row with >= 8192 entries) sum same-row runs in the
-// warp first — a COO record is sorted by (row, col), so a row's elements are adjacent
-// lanes — and the run's first lane issues the one RED; otherwise R-MAT's hub rows receive ~10^5
-// same-address atomics per SpMV, serialised in L2.
+// Chunks with runs (desc bit 2, set by the builder when two adjacent elements share a row — a
+// COO record is sorted by (row, col)) sum each run in the warp first and the run's
+// first lane issues the one RED; otherwise R-MAT's hub rows receive ~10^5 same-address atomics
+// per SpMV, serialised in L2.
 template <typename V, bool SCALED>
 __device__ __forceinline__ void coo_finish(const CooPend<V> &r, V scale, V *__restrict__ y, int lane, Dbg dbg) {
   V p = r.v * r.xv;
   if constexpr (SCALED) p *= scale;
-  if (r.hub) {  // warp-uniform (one descriptor)
+  if (r.runs) {  // warp-uniform (one descriptor)
     const uint32_t key = r.valid ? r.row : 0xFFFFFFFFu - (uint32_t)lane;  // invalid lanes: unique keys
     const uint32_t kn = __shfl_down_sync(kFull, key, 1);
     bool tail = lane == 31 || kn != key;  // last lane of its run
-    if (__any_sync(kFull, !tail)) {
+    {
       const uint32_t kp = __shfl_up_sync(kFull, key, 1);
       const bool head = lane == 0 || kp != key;
       // segmented suffix scan: p = sum over [lane, end of run]
@@ -618,11 +618,17 @@ int cb_configure(CbDevice *dev, std::string *err) {
   //   dynamic claiming for large aggregated matrices (per-page work follows the random gathers
   //   and atomics); strided static runs for 4-byte stored values (issue-bound: each CTA sees the
   //   slot order's whole format mix); contiguous byte-balanced ranges otherwise.
+  // Measured on B200: dynamic claims of runs of 16 pages beat static ranges on
+  // every large matrix (clustered fp64 0.745 -> 0.72 ms, fp32 0.58 -> 0.47 ms: Alg. 2's slot
+  // order puts the DENSE-heavy TBs first and the COO / CSR-heavy ones last, so equal byte ranges
+  // are unequal work; R-MAT 1.16 -> 1.13 ms); single pages dealt round robin lose DRAM locality
+  // (clustered 1.11 ms).  The claim shrinks for small matrices so the tail stays short.
   const int dyn_env = env_int("CBSPMV_DYNAMIC_PAGES", -1);
-  dev->dynamic = dyn_env >= 0 ? dyn_env != 0 : (dev->agg && dev->n_pages >= 32 * (int64_t)dev->grid);
-  dev->claim_chunk = (uint32_t)std::max(1, env_int("CBSPMV_CLAIM_CHUNK", 8));
+  dev->dynamic = dyn_env >= 0 ? dyn_env != 0 : dev->n_pages >= 64 * (int64_t)dev->grid;  // Laplacian (29 / CTA): static 0.027 vs dynamic 0.033 ms
+  const int64_t per = dev->n_pages / std::max<int64_t>(1, 16 * (int64_t)dev->grid);
+  dev->claim_chunk = (uint32_t)std::max(1, env_int("CBSPMV_CLAIM_CHUNK", (int)std::min<int64_t>(16, std::max<int64_t>(1, per))));
   const int str_env = env_int("CBSPMV_STRIDED_PAGES", -1);
-  dev->strided = dev->dynamic ? 0 : (str_env >= 0 ? str_env : (dev->dtype != CBSPMV_F64 ? 1 : 0));
+  dev->strided = dev->dynamic ? 0 : std::max(0, str_env);
   dev->dbg_skip = env_int("CBSPMV_DEBUG_SKIP", 0);
   return CBSPMV_OK;
 }

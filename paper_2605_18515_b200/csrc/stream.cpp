@@ -95,20 +95,13 @@ void free_stream(Stream *s) {
 }
 
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err, int64_t hub_nnz) {
+                 std::string *err, bool runs) {
   if (c.blk != 16) { *err = "the device page stream needs 16x16 blocks"; return CBSPMV_EUNSUPPORTED; }
   if (page_cap > kMaxPageCap || page_cap < 1024) { *err = "stage capacity out of range"; return CBSPMV_EUNSUPPORTED; }
   const int T = resolve_threads(threads);
   const int S = c.val_size;
   const Shape sh{S, x_size};
   PhaseTimer tm;
-  std::vector<uint8_t> hub;
-  if (hub_nnz > 0) {
-    std::vector<int64_t> brn((size_t)std::max<int64_t>(c.blk_m, 1), 0);
-    for (int64_t i = 0; i < c.nb; i++) brn[(size_t)c.br[i]] += c.nnzb[i];
-    hub.assign(brn.size(), 0);
-    for (size_t b = 0; b < brn.size(); b++) hub[b] = brn[b] >= hub_nnz;
-  }
   std::vector<int32_t> ncol((size_t)c.nb);
   std::vector<int64_t> rec((size_t)c.nb);  // CSR / DENSE: device record bytes (restore + record)
   parallel_for(c.nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
@@ -178,6 +171,8 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     plan->coo_lane.assign((size_t)c.nb, 0);
     plan->coo_member.assign((size_t)c.nb, 0);
     plan->chunk_off.assign((size_t)nchunks, 0);
+    plan->chunk_desc.assign((size_t)nchunks, 0);
+    plan->runs = runs;
     plan->chunk_nv.assign((size_t)nchunks, 0);
     plan->chunk_nm.assign((size_t)nchunks, 0);
   } else if (total > 0) {
@@ -201,10 +196,9 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
   parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
     std::vector<Piece> pieces;
     std::vector<int> cnv, cnm;           // per chunk of the page
-    std::vector<uint8_t> chub;
     std::vector<int64_t> cd;              // CSR / DENSE blocks of the page
     for (int64_t p = lo; p < hi; p++) {
-      pieces.clear(); cnv.clear(); cnm.clear(); chub.clear(); cd.clear();
+      pieces.clear(); cnv.clear(); cnm.clear(); cd.clear();
       PageAcc a;
       for (int64_t i = pb[p]; i < pb[p + 1]; i++) {
         if (c.type[i] != CBSPMV_FMT_COO) { cd.push_back(i); continue; }
@@ -216,13 +210,11 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
       if (a.nv) sh.close_chunk(a);
       cnv.assign((size_t)a.chunks, 0);
       cnm.assign((size_t)a.chunks, 0);
-      chub.assign((size_t)a.chunks, 0);
       for (const Piece &pc : pieces) {
         const size_t ch = (size_t)pc.chunk;
         const int t = pc.t;
         cnv[ch] = std::max(cnv[ch], pc.lane0 + t);
         cnm[ch] = std::max(cnm[ch], pc.member + 1);
-        if (!hub.empty() && hub[(size_t)c.br[pc.block]]) chub[ch] = 1;
       }
       const int64_t nch = (int64_t)cnv.size();
       const int64_t nitems = (int64_t)cd.size() + nch;
@@ -284,11 +276,12 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
         d[0] = (uint32_t)pos | ((uint32_t)cnv[ch] << 16) | ((uint32_t)cnm[ch] << 24);
         d[1] = (uint32_t)(pos + L.rows) | ((uint32_t)(pos + L.cols) << 16);
         d[2] = (uint32_t)(pos + L.vals);
-        d[3] = (uint32_t)CBSPMV_FMT_COO | (chub[ch] ? kDescHub : 0u);
+        d[3] = (uint32_t)CBSPMV_FMT_COO;  // the runs flag is set once the elements are in place
         std::memcpy(page + desc0 + kDescBytes * it, d, 16);
         it++;
         if (plan) {
           plan->chunk_off[chunk0[p] + ch] = off[p] + (uint64_t)pos;
+          plan->chunk_desc[chunk0[p] + ch] = off[p] + (uint64_t)(desc0 + kDescBytes * (it - 1));
           plan->chunk_nv[chunk0[p] + ch] = (uint8_t)cnv[ch];
           plan->chunk_nm[chunk0[p] + ch] = (uint8_t)cnm[ch];
         }
@@ -322,6 +315,27 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
           const uint32_t col = seg ? seg[b >> 4] : (uint32_t)c.bc[i] * (uint32_t)c.blk + (b >> 4);
           std::memcpy(r + L.cols + 4 * lane, &col, 4);
           std::memcpy(r + L.vals + (int64_t)S * lane, vals + e * S, (size_t)S);
+        }
+      }
+      // runs flag: two adjacent elements of a chunk share a global row (a COO record is sorted by
+      // (row, col), so a row's elements in one block are adjacent)
+      if (!plan && runs) {
+        for (int64_t ch = 0; ch < nch; ch++) {
+          const ChunkLayout L = chunk_layout(cnv[ch], cnm[ch], S);
+          const uint8_t *r = page + crec[ch];
+          uint32_t prev = 0xFFFFFFFFu;
+          bool run = false;
+          for (int l = 0; l < cnv[ch] && !run; l++) {
+            uint32_t rb;
+            std::memcpy(&rb, r + 4 * (r[L.rows + l] >> 4), 4);
+            const uint32_t row = rb + (r[L.rows + l] & 15);
+            run = row == prev;
+            prev = row;
+          }
+          if (run) {
+            uint32_t *dw = reinterpret_cast<uint32_t *>(page + desc0 + kDescBytes * ((int64_t)cd.size() + ch)) + 3;
+            *dw |= kDescRuns;
+          }
         }
       }
     }

@@ -171,7 +171,8 @@ def test_exact_integer_bitwise_device_built(pattern):
 
 @pytest.mark.parametrize("A", CORPUS[::3], ids=lambda A: A.name)
 def test_device_built_with_run_sums_forced(A, monkeypatch):
-    """The hub-row flag (desc.row0 bit 0) and the run-summing kernel on device-built handles."""
+    """The chunk runs flags (set on the device by k_chunk_flags) and the run sums on device-built
+    handles; the stream-decode test checks the flags themselves."""
     _ok()
     monkeypatch.setenv("CBSPMV_COO_RUNS", "1")
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=12)

@@ -246,7 +246,6 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
     agg = h.info["agg"]
     mtx, vp = ex["mtx_data"], ex["vp_per_blk"].astype(np.int64)
     nxt = 0
-    brn = np.bincount(ex["blk_row_idx"], weights=ex["nnz_per_blk"], minlength=1)
     for P in pages:
         pg = P["page"]
         assert P["blk0"] == nxt and P["nblk"] > 0
@@ -311,8 +310,7 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
             cols = pg[it["cols"]:it["cols"] + 4 * nv].view(np.uint32).astype(np.int64)
             vals = pg[it["vals"]:it["vals"] + S * nv].view(vdt)
             g = rb[rows >> 4] + (rows & 15)
-            if it["hub"]:
-                assert np.any(brn[g // 16] >= 8192)
+            assert it["hub"] == int(bool(np.any(g[1:] == g[:-1])))  # runs flag: adjacent equal rows
             got += list(zip(g.tolist(), cols.tolist(), vals.tolist()))
         assert got == want
     assert nxt == ex["nb"]
@@ -580,10 +578,11 @@ def test_spmv_host_batch_pipelined(count, dtype):
 
 @pytest.mark.parametrize("A", CORPUS[::2], ids=lambda A: A.name)
 @pytest.mark.parametrize("dtype", ["f64", "f32", "f32f64"])
-def test_coo_run_sums_forced_on(A, dtype, monkeypatch):
-    """The aggregated kernel variant that sums same-row runs of a COO group in the warp before
-    the RED (on automatically for hub block rows), forced on for the corpus."""
-    monkeypatch.setenv("CBSPMV_COO_RUNS", "1")
+@pytest.mark.parametrize("runs", ["0", "1"])
+def test_coo_run_sums_on_and_off(A, dtype, runs, monkeypatch):
+    """The in-warp sums of same-row runs of a COO chunk before the RED (chunks flagged by the
+    builder), and the same path with every flag off."""
+    monkeypatch.setenv("CBSPMV_COO_RUNS", runs)
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=5)
     for agg in (0, 1):
         y, h = gpu_spmv(A, x, dtype=dtype, agg_mode=agg)
@@ -597,8 +596,9 @@ def test_coo_run_sums_forced_on(A, dtype, monkeypatch):
 
 
 @pytest.mark.parametrize("pattern", ["random", "hub", "banded"])
-def test_coo_run_sums_exact_integer_bitwise(pattern, monkeypatch):
-    monkeypatch.setenv("CBSPMV_COO_RUNS", "1")
+@pytest.mark.parametrize("runs", ["0", "1"])
+def test_coo_run_sums_exact_integer_bitwise(pattern, runs, monkeypatch):
+    monkeypatch.setenv("CBSPMV_COO_RUNS", runs)
     A = synth.random_csr(300, 260, 0.08, 17, val_mode=2, pattern=pattern)
     x = synth.vector(A.n, synth.VEC_INT7)
     y_ref, _ = oracle.spmv_csr(A, x)
@@ -608,8 +608,8 @@ def test_coo_run_sums_exact_integer_bitwise(pattern, monkeypatch):
 
 
 def test_coo_run_sums_on_for_rmat_hubs():
-    """R-MAT has hub block rows (>= 8192 entries), so its build takes the run-summing kernel:
-    the 4096 lowest rows (the hubs) and a random sample against the oracle."""
+    """R-MAT's hub rows give many chunks same-row runs (flagged, summed in the warp): the 4096
+    lowest rows (the hubs) and a random sample against the oracle."""
     _ok()
     A = synth.make("rmat")
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=9)
