@@ -38,9 +38,15 @@ namespace cb {
 //                d[2,7) ncols (valid x-tile columns), d[8,16) nnz - 1, d[16,32) x tile offset
 //                in the stage (non-aggregated only: 16 values after the page, filled by TMA)
 //   COO chunk:   a = rowbase offset | nv << 16 | nm << 24; b = rows offset | cols offset << 16;
-//                c = values offset; d[2] runs flag (two adjacent elements share a global
-//                row: the kernel sums same-row runs in the warp before the RED)
+//                c = values offset; d[2,5) run steps: ceil(log2(longest run of adjacent
+//                elements sharing a global row)), 0 = no run; the kernel sums each run in the
+//                warp with that many shuffle steps before the RED
 // ---------------------------------------------------------------------------
+#ifdef __CUDACC__
+#define CB_HD __host__ __device__
+#else
+#define CB_HD
+#endif
 constexpr int kPageHeader = 16;
 constexpr int kDescBytes = 16;
 constexpr int kChunkLanes = 32;
@@ -48,13 +54,14 @@ constexpr int kChunkMembers = 16;          // member index is 4 bits of the row 
 constexpr uint32_t kEndItems = 0xFFFFFFFFu;  // header.nitems of the dynamic-claiming end marker
 constexpr int kMaxPageCap = 65536;         // descriptor offsets are u16 bytes
 constexpr int kCtrSlots = 64;              // page-claim counters per panel (launch k uses slot k % 64)
-constexpr uint32_t kDescRuns = 1u << 2;
+constexpr int kRunShift = 2;  // desc.d[2,5): run steps (0..5)
+// steps of a segmented warp sum covering runs of up to maxrun lanes: ceil(log2(maxrun))
+CB_HD inline uint32_t run_steps(int maxrun) {
+  uint32_t s = 0;
+  while ((1 << s) < maxrun) s++;
+  return s;
+}
 
-#ifdef __CUDACC__
-#define CB_HD __host__ __device__
-#else
-#define CB_HD
-#endif
 struct ChunkLayout {
   int rows, cols, vals, bytes;  // offsets from the chunk record start; total (16-aligned)
 };

@@ -563,7 +563,8 @@ __global__ void k_coo(int64_t nb, const int32_t *__restrict__ br, const int32_t 
   }
 }
 
-// one warp per chunk: the runs flag (two adjacent elements share a global row) into its descriptor
+// one warp per chunk: the run steps (ceil(log2(longest run of adjacent elements sharing a global
+// row))) into its descriptor
 __global__ void k_chunk_flags(int64_t nch, const uint64_t *__restrict__ chunk_off, const uint64_t *__restrict__ chunk_desc,
                               const uint8_t *__restrict__ chunk_nv, const uint8_t *__restrict__ chunk_nm, int S,
                               uint8_t *__restrict__ stream) {
@@ -580,8 +581,10 @@ __global__ void k_chunk_flags(int64_t nch, const uint64_t *__restrict__ chunk_of
       row = reinterpret_cast<const uint32_t *>(r)[b >> 4] + (b & 15);
     }
     const uint32_t prev = __shfl_up_sync(0xffffffffu, row, 1);
-    if (__any_sync(0xffffffffu, lane > 0 && lane < nv && prev == row) && lane == 0)
-      reinterpret_cast<uint32_t *>(stream + chunk_desc[ch])[3] |= kDescRuns;
+    const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || prev != row);
+    const int head = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // first lane of my run
+    const int maxrun = (int)__reduce_max_sync(0xffffffffu, (unsigned)(lane - head + 1));
+    if (lane == 0) reinterpret_cast<uint32_t *>(stream + chunk_desc[ch])[3] |= run_steps(maxrun) << kRunShift;
   }
 }
 

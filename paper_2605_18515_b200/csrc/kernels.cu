@@ -137,7 +137,8 @@ template <typename V>
 struct CooPend {
   V v, xv;
   uint32_t row;
-  bool valid, runs;
+  uint32_t steps;  // run-sum shuffle steps (0: no run)
+  bool valid;
 };
 
 template <typename M, typename V>
@@ -146,7 +147,7 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   CooPend<V> r;
   const int nv = (d.x >> 16) & 0xFF;
   r.valid = lane < nv;
-  r.runs = (d.w & cb::kDescRuns) != 0;
+  r.steps = (d.w >> cb::kRunShift) & 7;
   const uint8_t *rows = page + (d.y & 0xFFFFu);
   const uint32_t *cols = reinterpret_cast<const uint32_t *>(page + (d.y >> 16));
   const M *vals = reinterpret_cast<const M *>(page + (d.z & 0xFFFFu));
@@ -159,36 +160,50 @@ __device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4
   return r;
 }
 
-// Chunks with runs (desc bit 2, set by the builder when two adjacent elements share a row — a
-// COO record is sorted by (row, col)) sum each run in the warp first and the run's
-// first lane issues the one RED; otherwise R-MAT's hub rows receive ~10^5 same-address atomics
-// per SpMV, serialised in L2.
-template <typename V, bool SCALED>
-__device__ __forceinline__ void coo_finish(const CooPend<V> &r, V scale, V *__restrict__ y, int lane, Dbg dbg) {
-  V p = r.v * r.xv;
-  if constexpr (SCALED) p *= scale;
-  if (r.runs) {  // warp-uniform (one descriptor)
-    const uint32_t key = r.valid ? r.row : 0xFFFFFFFFu - (uint32_t)lane;  // invalid lanes: unique keys
-    const uint32_t kn = __shfl_down_sync(kFull, key, 1);
-    bool tail = lane == 31 || kn != key;  // last lane of its run
-    {
-      const uint32_t kp = __shfl_up_sync(kFull, key, 1);
-      const bool head = lane == 0 || kp != key;
-      // segmented suffix scan: p = sum over [lane, end of run]
+// Chunks with runs (desc steps > 0, set by the builder: ceil(log2(longest run of adjacent
+// elements sharing a row)) — a COO record is sorted by (row, col)) sum each run in the
+// warp first and the run's first lane issues the one RED; otherwise R-MAT's hub rows receive
+// ~10^5 same-address atomics per SpMV, serialised in L2.  The scan: one ballot of
+// the run ends gives every lane its run's last lane, then `steps` shuffle-adds (a run of up to
+// 2^steps lanes ends up summed on its first lane); a batch of B chunks scans together, so the
+// B shuffle chains overlap.
+template <typename V, bool SCALED, int B>
+__device__ __forceinline__ void coo_finish(const CooPend<V> (&q)[B], V scale, V *__restrict__ y, int lane, Dbg dbg) {
+  V p[B];
+  bool lead[B];
+  uint32_t steps = 0;
 #pragma unroll
-      for (int s = 1; s < 32; s <<= 1) {
-        const V o = __shfl_down_sync(kFull, p, s);
-        const bool ot = __shfl_down_sync(kFull, tail, s);
-        if (!tail && lane + s < 32) {
-          p += o;
-          tail = ot;
+  for (int j = 0; j < B; j++) {
+    p[j] = q[j].v * q[j].xv;
+    if constexpr (SCALED) p[j] *= scale;
+    lead[j] = q[j].valid;
+    steps = max(steps, q[j].steps);
+  }
+  if (steps) {  // warp-uniform: the batch's chunks scan together (B independent shuffle chains)
+    int rem[B];
+#pragma unroll
+    for (int j = 0; j < B; j++) {
+      const uint32_t key = q[j].valid ? q[j].row : 0xFFFFFFFFu - (uint32_t)lane;  // invalid lanes: unique keys
+      const uint32_t kn = __shfl_down_sync(kFull, key, 1);
+      const unsigned tails = __ballot_sync(kFull, lane == 31 || kn != key) | 0x80000000u;
+      rem[j] = q[j].steps ? __ffs(tails >> lane) - 1 : 0;  // lanes to the end of my run
+      lead[j] = q[j].valid && (lane == 0 || ((tails >> (lane - 1)) & 1u));  // first lane of its run
+    }
+#pragma unroll
+    for (int s = 0; s < 5; s++) {
+      if (s < (int)steps) {
+        const int d = 1 << s;
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+          const V o = __shfl_down_sync(kFull, p[j], d);
+          if (d <= rem[j]) p[j] += o;
         }
       }
-      if (r.valid && head) red_add(y + r.row, p, dbg);
-      return;
     }
   }
-  if (r.valid) red_add(y + r.row, p, dbg);
+#pragma unroll
+  for (int j = 0; j < B; j++)
+    if (lead[j]) red_add(y + q[j].row, p[j], dbg);
 }
 
 // Aggregated CSR / DENSE block: its x tile x[restore_cols[cols_offset[br] + bc*16 + c]]
@@ -470,7 +485,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   const int grp = cw / W, wg = cw - grp * W;
   int s = grp;
   uint32_t parity = 0;
-  int rot = 0;  // (items of this group's earlier pages) mod W
+  int kc = wg;  // this warp's first item of the group's next page (items continue across pages)
   for (uint32_t li = (uint32_t)grp; dyn || li < npl; li += (uint32_t)G) {
     mbar_wait(&full[s], parity);
     const uint8_t *page = ring + (size_t)s * P.stage;
@@ -480,8 +495,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
     const int n = (dbg.skip() & 4) ? 0 : (int)nitems;
     const int ncd = (int)reinterpret_cast<const uint32_t *>(page)[1];
-    int k = wg - rot;
-    if (k < 0) k += W;
+    int k = kc;
     // CSR / DENSE items first (the page lists them before the chunks)
     for (; k < ncd && k < n; k += W) {
       const uint4 d = descs[k];
@@ -495,11 +509,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       CooPend<V> q[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V>(page, descs[k + j * W], x, lane, xpol);
-#pragma unroll
-      for (int j = 0; j < 4; j++) coo_finish<V, SCALED>(q[j], scale, y, lane, dbg);
+      coo_finish<V, SCALED, 4>(q, scale, y, lane, dbg);
     }
-    for (; k < n; k += W) coo_finish<V, SCALED>(coo_issue<M, V>(page, descs[k], x, lane, xpol), scale, y, lane, dbg);
-    rot = (int)((rot + nitems) % (uint32_t)W);
+    for (; k < n; k += W) {
+      CooPend<V> q[1] = {coo_issue<M, V>(page, descs[k], x, lane, xpol)};
+      coo_finish<V, SCALED, 1>(q, scale, y, lane, dbg);
+    }
+    if (n != (int)nitems) k += ((int)nitems - k + W - 1) / W * W;  // ablation skipped the items
+    kc = k - (int)nitems;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     s += G;

@@ -317,25 +317,24 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
           std::memcpy(r + L.vals + (int64_t)S * lane, vals + e * S, (size_t)S);
         }
       }
-      // runs flag: two adjacent elements of a chunk share a global row (a COO record is sorted by
-      // (row, col), so a row's elements in one block are adjacent)
+      // run steps: the longest run of adjacent elements sharing a global row (a COO record is
+      // sorted by (row, col), so a row's elements in one block are adjacent)
       if (!plan && runs) {
         for (int64_t ch = 0; ch < nch; ch++) {
           const ChunkLayout L = chunk_layout(cnv[ch], cnm[ch], S);
           const uint8_t *r = page + crec[ch];
           uint32_t prev = 0xFFFFFFFFu;
-          bool run = false;
-          for (int l = 0; l < cnv[ch] && !run; l++) {
+          int len = 0, maxrun = 1;
+          for (int l = 0; l < cnv[ch]; l++) {
             uint32_t rb;
             std::memcpy(&rb, r + 4 * (r[L.rows + l] >> 4), 4);
             const uint32_t row = rb + (r[L.rows + l] & 15);
-            run = row == prev;
+            len = row == prev ? len + 1 : 1;
+            maxrun = std::max(maxrun, len);
             prev = row;
           }
-          if (run) {
-            uint32_t *dw = reinterpret_cast<uint32_t *>(page + desc0 + kDescBytes * ((int64_t)cd.size() + ch)) + 3;
-            *dw |= kDescRuns;
-          }
+          uint32_t *dw = reinterpret_cast<uint32_t *>(page + desc0 + kDescBytes * ((int64_t)cd.size() + ch)) + 3;
+          *dw |= run_steps(maxrun) << kRunShift;
         }
       }
     }

@@ -217,7 +217,7 @@ def decode_stream(stream, page_off):
             if t == 0:
                 nv, nm = (a >> 16) & 0xFF, a >> 24
                 items.append(dict(type=0, rb=a & 0xFFFF, nv=nv, nm=nm, rows=b & 0xFFFF, cols=b >> 16,
-                                  vals=c & 0xFFFF, hub=(d >> 2) & 1, xslot=xslot))
+                                  vals=c & 0xFFFF, steps=(d >> 2) & 7, xslot=xslot))
             else:
                 items.append(dict(type=t, row0=a, xinfo=b, body=c & 0xFFFF, vals=c >> 16, ncols=(d >> 2) & 31,
                                   nnz=((d >> 8) & 0xFF) + 1, xslot=xslot))
@@ -310,7 +310,10 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
             cols = pg[it["cols"]:it["cols"] + 4 * nv].view(np.uint32).astype(np.int64)
             vals = pg[it["vals"]:it["vals"] + S * nv].view(vdt)
             g = rb[rows >> 4] + (rows & 15)
-            assert it["hub"] == int(bool(np.any(g[1:] == g[:-1])))  # runs flag: adjacent equal rows
+            # run steps: ceil(log2(longest run of adjacent elements sharing a row))
+            brk = np.flatnonzero(np.diff(g) != 0)
+            maxrun = int(np.max(np.diff(np.concatenate([[-1], brk, [len(g) - 1]]))))
+            assert it["steps"] == int(np.ceil(np.log2(maxrun))) if maxrun > 1 else it["steps"] == 0
             got += list(zip(g.tolist(), cols.tolist(), vals.tolist()))
         assert got == want
     assert nxt == ex["nb"]
