@@ -135,28 +135,52 @@ __device__ __forceinline__ V ldg_x(const V *p, uint64_t pol) {
 // (member << 4 | local row) indexes the chunk's member row bases.
 template <typename V>
 struct CooPend {
-  V v, xv;
+  V v, xv;         // invalid lanes (>= nv) carry garbage: never summed into a run, never added
   uint32_t row;
-  uint32_t steps;  // run-sum shuffle steps (0: no run)
+  uint32_t steps;  // run-sum shuffle steps (0: no run), warp-uniform
   bool valid;
 };
 
+// 32-bit shared-memory loads (the page lives in the CTA's shared window: no 64-bit generic
+// address arithmetic per element)
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+template <typename M>
+__device__ __forceinline__ M lds_val(uint32_t a) {
+  M v;
+  if constexpr (sizeof(M) == 8) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  else asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+// pg: shared address of the page; da: shared address of the chunk's descriptor
 template <typename M, typename V>
-__device__ __forceinline__ CooPend<V> coo_issue(const uint8_t *page, const uint4 &d, const V *__restrict__ x,
-                                                int lane, uint64_t pol) {
+__device__ __forceinline__ CooPend<V> coo_issue(uint32_t pg, uint32_t da, const V *__restrict__ x, int lane,
+                                                uint64_t pol) {
   CooPend<V> r;
+  const uint4 d = lds_v4(da);
   const int nv = (d.x >> 16) & 0xFF;
   r.valid = lane < nv;
   r.steps = (d.w >> cb::kRunShift) & 7;
-  const uint8_t *rows = page + (d.y & 0xFFFFu);
-  const uint32_t *cols = reinterpret_cast<const uint32_t *>(page + (d.y >> 16));
-  const M *vals = reinterpret_cast<const M *>(page + (d.z & 0xFFFFu));
-  const uint32_t *rb = reinterpret_cast<const uint32_t *>(page + (d.x & 0xFFFFu));
-  const int l = r.valid ? lane : 0;  // invalid lanes re-read element 0 (never used)
-  const uint32_t rbyte = rows[l];
-  r.v = V(vals[l]);
-  r.xv = ldg_x(x + cols[l], pol);
-  r.row = rb[rbyte >> 4] + (rbyte & 15);
+  const uint32_t l = (uint32_t)min(lane, nv - 1);  // invalid lanes re-read the last element
+  const uint32_t rbyte = lds_u8(pg + (d.y & 0xFFFFu) + l);
+  const uint32_t col = lds_u32(pg + (d.y >> 16) + 4 * l);
+  r.v = V(lds_val<M>(pg + (d.z & 0xFFFFu) + (uint32_t)sizeof(M) * l));
+  r.xv = ldg_x(x + col, pol);
+  r.row = lds_u32(pg + (d.x & 0xFFFFu) + 4 * (rbyte >> 4)) + (rbyte & 15);
   return r;
 }
 
@@ -505,15 +529,24 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       else dense_path<M, V, SCALED>(page, d, xt, scale, y, P.m, lane, dbg);
     }
     // COO chunks, four at a time: the four chunks' loads and x gathers in flight together
+    const uint32_t pg = smem_addr(page), dsc = pg + cb::kPageHeader;
     for (; k + 3 * W < n; k += 4 * W) {
       CooPend<V> q[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V>(page, descs[k + j * W], x, lane, xpol);
+      for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol);
       coo_finish<V, SCALED, 4>(q, scale, y, lane, dbg);
     }
-    for (; k < n; k += W) {
-      CooPend<V> q[1] = {coo_issue<M, V>(page, descs[k], x, lane, xpol)};
+    if (k + W < n) {
+      CooPend<V> q[2];
+#pragma unroll
+      for (int j = 0; j < 2; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol);
+      coo_finish<V, SCALED, 2>(q, scale, y, lane, dbg);
+      k += 2 * W;
+    }
+    if (k < n) {
+      CooPend<V> q[1] = {coo_issue<M, V>(pg, dsc + 16u * (uint32_t)k, x, lane, xpol)};
       coo_finish<V, SCALED, 1>(q, scale, y, lane, dbg);
+      k += W;
     }
     if (n != (int)nitems) k += ((int)nitems - k + W - 1) / W * W;  // ablation skipped the items
     kc = k - (int)nitems;
