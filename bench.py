@@ -103,15 +103,27 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workload
 def make_matrix(config: str, rank: int, world: int):
-    """Generate this rank's row shard (rows split by nnz at block-row boundaries)."""
+    """This rank's row shard, generated alone ("each rank generates and builds only
+    its rows"): the cut comes from per-row counts (synth.row_counts, no matrix materialised;
+    rows split by nnz at block-row boundaries, equal shards for the uniform matrix), then the
+    counter-based generator produces rows [r0, r1) only.  Returns (shard, (r0, r1), total nnz);
+    the total is all-reduced by the caller when world > 1."""
+    import numpy as np
     import synth
     from paper_2605_18515_b200 import dist
-    A = synth.make(config)
     if world == 1:
+        A = synth.make(config)
         return A, (0, A.m), A.nnz
-    cuts = dist.equal_bounds(A.m, world) if config == "uniform" else dist.shard_bounds(A.row_ptr, world)
+    counts = synth.row_counts(config)
+    if config == "uniform":
+        cuts = dist.equal_bounds(len(counts), world)
+    else:
+        rp = np.zeros(len(counts) + 1, np.int64)
+        np.cumsum(counts, out=rp[1:])
+        cuts = dist.shard_bounds(rp, world)
     r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
-    return dist.slice_rows(A, r0, r1), (r0, r1), A.nnz
+    S = synth.make(config, r0, r1)
+    return S, (r0, r1), None
 
 
 def peaks():
@@ -216,6 +228,8 @@ def run_cb(args, rank: int, world: int, local_rank: int):
     t0 = time.perf_counter()
     A, (r0, r1), nnz_total = make_matrix(args.config, rank, world)
     gen_s = time.perf_counter() - t0
+    if nnz_total is None:
+        nnz_total = int(allreduce(np.array([A.nnz], np.int64))[0])
     agg = dist.global_agg(A, lambda a: allreduce(a), dtype=args.dtype) if world > 1 else -1
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0)
@@ -267,6 +281,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
         cold.append(c0.elapsed_time(c1))
     del flush
     cold_ms = statistics.median(cold) if cold else None
+    cold_ms_max = float(allreduce(np.array([cold_ms or 0.0]), "max")[0])
 
     # ---- end to end through the public API with host buffers (pinned)
     # K independent requests (a ring of 4 pinned x / y host buffers) through
@@ -294,7 +309,8 @@ def run_cb(args, rank: int, world: int, local_rank: int):
     value = flops / (ms_max * 1e-3) / 1e9
     peak, peak_src = peaks()
     achieved = info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config, args.dtype)
+    # ncu DRAM bytes of the whole-matrix launch (profiles/ncu_traffic.json): only a 1-GPU line
+    traffic = ncu_traffic(args.config, args.dtype) if world == 1 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -317,7 +333,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
                 **({"shared_gpu_test": True} if shared_gpu_test() else {}),
                 "l2": "inputs larger than L2 (matrix stream %.2f GB vs 126 MB L2); cold_l2_ms flushes 512 MB "
                       "before each step" % (info["dev_stream_bytes"] / 1e9),
-                "cold_l2_ms": cold_ms, "cold_l2_gflops": flops / (cold_ms * 1e-3) / 1e9 / world if cold_ms else None,
+                "cold_l2_ms": cold_ms, "cold_l2_gflops": flops / (cold_ms_max * 1e-3) / 1e9 if cold_ms else None,
                 "alg_bytes_per_spmv": int(info["alg_bytes"]), "dev_stream_bytes": int(info["dev_stream_bytes"]),
                 "achieved_hbm_gbs_step": info["alg_bytes"] / (ms * 1e-3) / 1e9,
                 "tb_load_sd": info["tb_load_sd"], "tb_load_sd_natural": info["tb_load_sd_natural"],
@@ -405,6 +421,8 @@ def run_power(args, rank, world, local_rank):
     t0 = time.perf_counter()
     A, (r0, r1), nnz_total = make_matrix("uniform", rank, world)
     gen_s = time.perf_counter() - t0
+    if nnz_total is None:
+        nnz_total = int(_allreduce_np(np.array([A.nnz], np.int64), cdev, world)[0])
     agg = dist.global_agg(A, lambda a: _allreduce_np(a, cdev, world), dtype=args.dtype) if world > 1 else -1
     # column panels: the auto count on one GPU (x slices L2-resident); with N ranks a multiple
     # of N so panel cuts fall on the x owners' boundaries (NEXT-1 (i) overlap)
@@ -449,6 +467,46 @@ def run_power(args, rank, world, local_rank):
     torch.cuda.synchronize()
     kernel_ms = k0.elapsed_time(k1) / args.steps
     lam = float(ss.item()) ** 0.5
+    # per-step split (fused exchange): CUDA events after each enqueued phase of a separate run
+    split = None
+    if fused is not None:
+        marks = []
+
+        def mark(phase):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(st)
+            marks.append((phase, ev))
+        fused.run(x0, args.steps, mark=mark)
+        torch.cuda.synchronize()
+        acc = {}
+        for (_, a), (ph, b) in zip(marks[:-1], marks[1:]):
+            acc[ph] = acc.get(ph, 0.0) + a.elapsed_time(b)
+        split = {k + "_ms": v / args.steps for k, v in acc.items()}
+        split["note"] = ("per step, CUDA events on the stream after each enqueued phase: wait = device flag wait "
+                         "for every rank's publish of the previous step (+ rank-order sum of squares), spmv = "
+                         "zero y + the panels' SpMV kernels, publish = the fused finalize / peer-store kernel")
+    # end to end through the public API: the start vector from pinned host memory, K steps, the
+    # eigenvalue estimate read back (what a user of the power iteration gets)
+    e2e = None
+    if fused is not None:
+        x0_host = torch.ones(A.n, dtype=tdt).pin_memory()
+        if world > 1:
+            tdist.barrier()
+        t_e = time.perf_counter()
+        x0_dev = x0_host.to(dev, non_blocking=True)
+        _, ss_e = fused.run(x0_dev, args.steps)
+        lam_e = float(ss_e.item()) ** 0.5
+        e2e_s = time.perf_counter() - t_e
+        e2e_max = float(_allreduce_np(np.array([e2e_s]), cdev, world, "max")[0])
+        e2e = {"value": 2.0 * nnz_total * args.steps / e2e_max / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(A.n) * x0_host.element_size() / args.steps,
+               "d2h_bytes_per_step": 8 / args.steps, "lambda": lam_e,
+               "path": f"x0 from pinned host memory -> FusedPowerIteration.run({args.steps} steps) -> lambda read "
+                       "back; host copies inside the timed region, amortised over the steps"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(A, np.ones(A.n), args.dtype)
+        cpu["sample"] += " of this rank's rows, one SpMV of the power iteration"
     if fused is not None and fused.timed_out():
         raise RuntimeError("fused exchange: a device wait timed out (a peer never published)")
     peak, peak_src = peaks()
@@ -461,6 +519,7 @@ def run_power(args, rank, world, local_rank):
                        "name": "uniform", "nnz": int(nnz_total), "rows_per_rank": int(A.m), "agg": int(info["agg"]),
                        "lambda": lam, "gen_s": gen_s, "build_s": info["build_seconds"],
                        "n_panels": int(info["n_panels"]), "gather_floor": gather_floor(info, kernel_ms),
+                       "step_split": split, "rows_per_rank_range": [int(r0), int(r1)],
                        "exchange": args.exchange,
                        **({"shared_gpu_test": True} if shared_gpu_test() else {}),
                        "parallelism": f"row-shard x{world}, " + {
@@ -470,12 +529,13 @@ def run_power(args, rank, world, local_rank):
                                "nccl" if args.no_overlap else args.exchange]},
             "roofline": {"bound": "hbm", "achieved": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": info["alg_bytes"] / (kernel_ms * 1e-3) / 1e9 / peak,
-                         "traffic": ncu_traffic("uniform", args.dtype), "kernel": "cb_spmv_kernel",
+                         "traffic": ncu_traffic("uniform", args.dtype) if world == 1 else None,
+                         "kernel": "cb_spmv_kernel",
                          "kernel_ms": kernel_ms, "peak_source": peak_src},
             "gpu_launches": int(args.steps * ((3 + info["n_panels"]) if args.exchange == "fused" else
                                               (2 + (1 if args.no_overlap else info["n_panels"])))),
-            "clocks": clk.summary(), "cpu_baseline": None,
-            "e2e": None,
+            "clocks": clk.summary(), "cpu_baseline": cpu,
+            "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
     if fused is not None:

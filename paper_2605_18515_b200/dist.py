@@ -265,16 +265,24 @@ class PeerPowerIteration:
         self.row_bounds = check_row_bounds(rb, rb[-1][1] if n is None else n)
         self.rank = rank
 
-    def run(self, X, sumsq, steps: int, on_step=None, k0: int = 0):
+    def run(self, X, sumsq, steps: int, on_step=None, k0: int = 0, mark=None):
         """X: the two iterate buffers with x_{k0} in X[k0 & 1]; sumsq: ||x_{k0}||^2.
+        mark(phase) (optional) is called after each enqueued phase ("wait", "spmv", "publish"),
+        e.g. to record CUDA events for a per-phase time split.
         Returns (x_{k0+steps}, sumsq), complete on every rank."""
         r0, r1 = self.row_bounds[self.rank]
         for k in range(k0, k0 + steps):
             if k > k0:
                 self.wait(k, sumsq)
+                if mark is not None:
+                    mark("wait")
             cur, nxt = X[k & 1], X[(k + 1) & 1]
             self.spmv_scaled(cur, sumsq, nxt[r0:r1])
+            if mark is not None:
+                mark("spmv")
             self.publish((k + 1) & 1, r0, r1 - r0, k + 1)
+            if mark is not None:
+                mark("publish")
             if on_step is not None:
                 self.wait(k + 1, sumsq)  # debugging / tests: a complete iterate costs the overlap
                 on_step(k - k0, nxt, sumsq)
@@ -324,12 +332,14 @@ class FusedPowerIteration:
         if world > 1:
             tdist.barrier(group=group)  # every peer mapped before anyone stores into it
 
-    def run(self, x0, steps: int, on_step=None):
+    def run(self, x0, steps: int, on_step=None, mark=None):
         import paper_2605_18515_b200 as cb
         # safe to overwrite X[k & 1]: every peer's last store into it preceded our last wait(k)
         self.X[self.k & 1].copy_(x0)
         cb.sumsq(self.X[self.k & 1], self.ss, device=self.device)
-        x, ss = self.it.run(self.X, self.ss, steps, on_step=on_step, k0=self.k)
+        if mark is not None:
+            mark("start")
+        x, ss = self.it.run(self.X, self.ss, steps, on_step=on_step, k0=self.k, mark=mark)
         self.k += steps
         if self.xc.timed_out():  # synchronous status read: the run's waits have all executed
             raise RuntimeError("fused exchange: a device wait timed out (a peer never published); "

@@ -52,6 +52,9 @@ def _load():
         lib.synth_vector.argtypes = [i64, i64, c_int, u64, ctypes.POINTER(ctypes.c_double)]
         lib.synth_free.argtypes = [P]
         lib.synth_set_threads.argtypes = [c_int]
+        PI = ctypes.POINTER(ctypes.c_int64)
+        lib.synth_rmat_row_counts.argtypes = [c_int, i64, u64, PI]
+        lib.synth_clustered_row_counts.argtypes = [i64, i64, u64, PI]
         _lib = lib
     return _lib
 
@@ -128,6 +131,34 @@ def uniform(m: int, n: int | None = None, k: int = 50, seed: int = 51, val_mode:
     st = _CSR()
     _check(_load().synth_uniform(m, n, k, seed, val_mode, r0, r1, ctypes.byref(st)), "uniform")
     return _take(st, r0, f"uniform_m{m}_k{k}")
+
+
+def row_counts(name: str, small: bool = False) -> np.ndarray:
+    """Stored entries per row of ``make(name, small=small)`` without generating the matrix (the
+    counts a row-shard cut needs before each rank generates only its rows).  Exact for laplace,
+    clustered and uniform; for rmat the edge count per row before duplicate removal (an upper
+    bound: the cut it gives is balanced to within the duplicate rate)."""
+    L = _load()
+    if name == "laplace":
+        g = 100 if small else 1000
+        i, j = np.divmod(np.arange(g * g, dtype=np.int64), g)
+        return 1 + (i > 0) + (i < g - 1) + (j > 0) + (j < g - 1)
+    if name == "uniform":
+        m = (1 << 15) if small else (1 << 25)
+        return np.full(m, 50, np.int64)
+    if name == "clustered":
+        m = (1 << 14) if small else (1 << 22)
+        out = np.empty(m, np.int64)
+        _check(L.synth_clustered_row_counts(m, m, 41, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+               "clustered_row_counts")
+        return out
+    if name == "rmat":
+        scale = 14 if small else 23
+        out = np.empty(1 << scale, np.int64)
+        _check(L.synth_rmat_row_counts(scale, 16, 31, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+               "rmat_row_counts")
+        return out
+    raise ValueError(name)
 
 
 VEC_UNIFORM, VEC_ONES, VEC_INT7, VEC_FIG1 = 0, 1, 2, 3

@@ -228,6 +228,21 @@ int synth_rmat(int scale, int64_t edge_factor, uint64_t seed, int val_mode, int6
   return 0;
 }
 
+/* Per-row stored-entry counts of the whole matrix without materialising it (row shards are cut
+ * by nnz before each rank generates only its own rows).  R-MAT: edges per row before duplicate
+ * removal (an upper bound, exact enough to balance a cut). */
+int synth_rmat_row_counts(int scale, int64_t edge_factor, uint64_t seed, int64_t *counts) {
+  int64_t m = (int64_t)1 << scale, E = edge_factor * m;
+  if (scale < 1 || scale > 30) return -1;
+  int64_t *tmp = (int64_t *)calloc((size_t)m + 1, sizeof(int64_t));
+  if (!tmp) return -2;
+  rmatctx_t c = {seed, scale, 0, m, tmp, NULL, NULL};
+  parallel_for(E, rmat_count, &c);
+  memcpy(counts, tmp + 1, (size_t)m * sizeof(int64_t));
+  free(tmp);
+  return 0;
+}
+
 /* ---------------------------------------------------------------- clustered */
 /* One 16-row block row: up to 14 blocks x 256 entries, emitted row by row. */
 #define CL_BLOCKS 14
@@ -297,6 +312,16 @@ int synth_clustered(int64_t m, int64_t n, uint64_t seed, int val_mode, int64_t r
   c.col = A->col; c.counting = 0;
   parallel_for(nbr, cl_work, &c);
   values(A, r0, val_mode, seed + 1);
+  return 0;
+}
+
+int synth_clustered_row_counts(int64_t m, int64_t n, uint64_t seed, int64_t *counts) {
+  int64_t *tmp = (int64_t *)calloc((size_t)m + 1, sizeof(int64_t));
+  if (!tmp) return -2;
+  clctx_t c = {seed, m, n, 0, m, tmp, NULL, 1};
+  parallel_for((m + 15) / 16, cl_work, &c);
+  memcpy(counts, tmp + 1, (size_t)m * sizeof(int64_t));
+  free(tmp);
   return 0;
 }
 

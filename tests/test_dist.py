@@ -339,3 +339,27 @@ def test_row_bounds_must_tile_the_iterate():
         cbd.gather_row_bounds(999, 1000, 1)
     with pytest.raises(ValueError):  # the protocol driver refuses shards that leave a gap
         cbd.PeerPowerIteration(None, None, None, row_bounds=[(0, 10), (12, 20)], rank=0)
+
+
+@pytest.mark.parametrize("name", ["laplace", "clustered", "rmat", "uniform"])
+def test_row_counts_cut_and_per_rank_generation(name):
+    """bench.py's N > 1 input path: per-row counts without materialising the matrix, an nnz cut
+    at block-row boundaries, then each rank generates only its rows — identical to slicing the
+    full matrix (counter-based generators)."""
+    A = synth.make(name, small=True)
+    c = synth.row_counts(name, small=True)
+    d = np.diff(A.row_ptr)
+    assert len(c) == A.m
+    if name == "rmat":  # edges per row before duplicate removal: an upper bound
+        assert np.all(c >= d) and c.sum() <= 1.2 * d.sum()
+    else:
+        assert np.array_equal(c, d)
+    rp = np.zeros(len(c) + 1, np.int64)
+    np.cumsum(c, out=rp[1:])
+    cuts = cbd.equal_bounds(A.m, 3) if name == "uniform" else cbd.shard_bounds(rp, 3)
+    for r in range(3):
+        r0, r1 = int(cuts[r]), int(cuts[r + 1])
+        S = synth.make(name, r0, r1, small=True)
+        ref = cbd.slice_rows(A, r0, r1)
+        assert S.m == r1 - r0 and np.array_equal(S.row_ptr, ref.row_ptr)
+        assert np.array_equal(S.col, ref.col) and np.array_equal(S.val, ref.val)
