@@ -59,7 +59,44 @@ tools/mbm: tools/mb_mixed.cu
 tools/mbga: tools/mb_gather4_align.cu
 	$(NVCC) $(ARCH) -O3 -o $@ $< -lcuda
 
+# ASan + UBSan builds of the host code (builder, stream, C ABI, Matrix Market parser, CBSM loader,
+# oracle, generators) and `make asan-test`: the CPU test suite against them.
+ASAN_DIR   := build/asan
+ASAN_CC    := /usr/bin/gcc
+ASAN_CXX   := /usr/bin/g++
+ASAN_FLAGS := -fsanitize=address,undefined -fno-omit-frame-pointer -fno-sanitize-recover=undefined -g -O1
+ASAN_NVX   := -ccbin $(ASAN_CXX) -Xcompiler -fsanitize=address -Xcompiler -fsanitize=undefined -Xcompiler -fno-omit-frame-pointer
+ASAN_OBJS  := $(patsubst $(CSRC)/%.o,$(ASAN_DIR)/%.o,$(HOST_OBJS)) $(ASAN_DIR)/kernels.o $(ASAN_DIR)/gpu_builder.o $(ASAN_DIR)/exchange.o
+
+asan: $(ASAN_DIR)/libcbspmv.so $(ASAN_DIR)/liboracle.so $(ASAN_DIR)/libsynth.so
+
+$(ASAN_DIR)/libsynth.so: synth/synth.c
+	@mkdir -p $(ASAN_DIR)
+	$(ASAN_CC) $(ASAN_FLAGS) -fPIC -shared -Wall -pthread -o $@ $<
+
+$(ASAN_DIR)/liboracle.so: oracle/oracle.c
+	@mkdir -p $(ASAN_DIR)
+	$(ASAN_CC) $(ASAN_FLAGS) -fPIC -shared -Wall -Wextra -std=c11 -o $@ $<
+
+$(ASAN_DIR)/%.o: $(CSRC)/%.cpp $(CSRC)/cb_internal.h include/cbspmv.h
+	@mkdir -p $(ASAN_DIR)
+	$(ASAN_CXX) $(CXXFLAGS) $(ASAN_FLAGS) -c -o $@ $<
+
+$(ASAN_DIR)/%.o: $(CSRC)/%.cu $(CSRC)/cb_internal.h include/cbspmv.h
+	@mkdir -p $(ASAN_DIR)
+	$(NVCC) $(NVFLAGS) $(ASAN_NVX) -c -o $@ $< 2> /dev/null
+
+$(ASAN_DIR)/libcbspmv.so: $(ASAN_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lpthread $(ASAN_NVX)
+
+ASAN_RT := $(shell $(ASAN_CC) -print-file-name=libasan.so) $(shell $(ASAN_CC) -print-file-name=libubsan.so)
+asan-test: asan
+	ASAN_OPTIONS=detect_leaks=0:protect_shadow_gap=0:halt_on_error=1 UBSAN_OPTIONS=print_stacktrace=1 \
+	LD_PRELOAD="$(ASAN_RT)" CBSPMV_LIB=$(ASAN_DIR)/libcbspmv.so ORACLE_LIB=$(ASAN_DIR)/liboracle.so \
+	SYNTH_LIB=$(ASAN_DIR)/libsynth.so python -m pytest tests -m "not gpu" -q -x -p no:cacheprovider $(ASAN_PYTEST)
+
 clean:
 	rm -f synth/libsynth.so oracle/liboracle.so $(LIB) $(CSRC)/*.o $(CSRC)/ptxas*.log
+	rm -rf $(ASAN_DIR)
 
-.PHONY: all synth oracle lib tools clean
+.PHONY: all synth oracle lib tools clean asan asan-test

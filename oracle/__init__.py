@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_LIB_PATH = os.environ.get("ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")  # override: sanitizer builds (make asan)
 _lib = None
 
 FMT_COO, FMT_CSR, FMT_DENSE = 0, 1, 2

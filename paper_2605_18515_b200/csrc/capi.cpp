@@ -151,6 +151,7 @@ static void free_device(cbspmv_s *h) {
 // Device page stream of one panel's canonical format, uploaded in one copy (a8).
 static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Part *P, double *t_up,
                        std::string *err) {
+  cb::NvtxRange nvtx_("cbspmv upload (stream plan + one copy)");
   const cb::Canon &c = P->canon;
   cb::Stream S;
   CbShape shape;
@@ -231,6 +232,7 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
 // Build + upload one panel's format (the Fig. 7 pipeline on A[:, c0:c1)).
 static int build_part(const cb::Csr &A, const cbspmv_options_t &o, int dtype, cudaStream_t cs, Part *P,
                       double *t_up, std::string *err) {
+  cb::NvtxRange nvtx_("cbspmv build (a1..a7)");
   int st;
   if (o.device >= 0 && o.device_build) {
     P->dc.reset(new cb::DevCanon());
@@ -475,6 +477,7 @@ static int launch_all(cbspmv_handle_t h, const void *x, void *y, const double *s
 }
 
 static cbspmv_status_t run(cbspmv_handle_t h, const void *x, void *y, const double *ss, bool zero, void *stream) {
+  cb::NvtxRange nvtx_("cbspmv_spmv");
   cbspmv_status_t s = check_dev(h, x, y, ss);
   if (s != CBSPMV_OK) return s;
   DeviceGuard g(h->device);
@@ -499,6 +502,7 @@ cbspmv_status_t cbspmv_spmv_scaled(cbspmv_handle_t h, const void *x, const doubl
 
 cbspmv_status_t cbspmv_spmv_panel(cbspmv_handle_t h, int32_t k, const void *x, const double *sumsq, void *y,
                                   int32_t zero_y, void *stream) {
+  cb::NvtxRange nvtx_("cbspmv_spmv_panel");
   cbspmv_status_t s = check_dev(h, x, y, sumsq);
   if (s != CBSPMV_OK) return s;
   if (k < 0 || k >= (int32_t)h->parts.size()) return fail(CBSPMV_EINVAL, "panel index out of range");
@@ -518,6 +522,7 @@ cbspmv_status_t cbspmv_panel_bounds(cbspmv_handle_t h, int32_t k, int64_t *c0, i
 }
 
 cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_host, void *stream) {
+  cb::NvtxRange nvtx_("cbspmv_spmv_host");
   if (!h) return fail(CBSPMV_EINVAL, "null handle");
   if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle");
   if ((h->info.n > 0 && !x_host) || (h->info.m > 0 && !y_host)) return fail(CBSPMV_EINVAL, "null x or y");
@@ -541,6 +546,7 @@ cbspmv_status_t cbspmv_spmv_host(cbspmv_handle_t h, const void *x_host, void *y_
 
 cbspmv_status_t cbspmv_spmv_host_batch(cbspmv_handle_t h, const void *const *x_host, void *const *y_host,
                                        int64_t count, void *stream) {
+  cb::NvtxRange nvtx_("cbspmv_spmv_host_batch");
   if (!h) return fail(CBSPMV_EINVAL, "null handle");
   if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle");
   if (count < 0 || (count > 0 && (!x_host || !y_host))) return fail(CBSPMV_EINVAL, "bad batch arguments");

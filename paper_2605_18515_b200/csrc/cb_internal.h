@@ -13,7 +13,17 @@
 
 #include "cbspmv.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost ~nothing without a profiler attached
+
 namespace cb {
+
+// NVTX range for the scope (build / upload / SpMV / exchange phases show up in nsys / ncu timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ---------------------------------------------------------------------------
 // Device page stream, version 2.  A derived layout of the canonical format:

@@ -252,6 +252,7 @@ void *cbspmv_xchg_buffer(cbspmv_xchg_t x, int32_t b) {
 }
 
 cbspmv_status_t cbspmv_xchg_publish(cbspmv_xchg_t x, int32_t b, int64_t r0, int64_t len, uint64_t seq, void *stream) {
+  cb::NvtxRange nvtx_("cbspmv_xchg_publish");
   if (!x || (b != 0 && b != 1) || r0 < 0 || len < 0 || r0 + len > x->n || seq == 0)
     return (cbspmv_status_t)cb_set_error(CBSPMV_EINVAL, "bad publish arguments");
   for (int q = 0; q < x->world; q++)
@@ -272,6 +273,7 @@ cbspmv_status_t cbspmv_xchg_publish(cbspmv_xchg_t x, int32_t b, int64_t r0, int6
 }
 
 cbspmv_status_t cbspmv_xchg_wait(cbspmv_xchg_t x, uint64_t seq, double *sumsq_dev, double timeout_s, void *stream) {
+  cb::NvtxRange nvtx_("cbspmv_xchg_wait");
   if (!x || !sumsq_dev || seq == 0) return (cbspmv_status_t)cb_set_error(CBSPMV_EINVAL, "bad wait arguments");
   Guard g(x->device);
   const double t = timeout_s > 0 ? timeout_s : 10.0;
