@@ -14,6 +14,23 @@ cases = [(synth.fig1(), {}), (synth.rmat(10, 16, 3), {}), (synth.clustered(1 << 
          (synth.random_csr(50, 50, 0.4, 4, pattern="blockdense"), {"force_format": 2}),
          (synth.random_csr(50, 600, 0.2, 5), {"col_panels": 3}),
          (synth.uniform(1 << 10, 1 << 10, 20, 5, 1), {"agg_mode": 0})]
+# stage reuse (many 4 KB pages per CTA), with dynamic and static page claiming
+reuse = [(synth.clustered(1 << 13), {}), (synth.rmat(12, 16, 3), {})]
+for env in ({"CBSPMV_PAGE_BYTES": "4096", "CBSPMV_DYNAMIC_PAGES": "1"},
+            {"CBSPMV_PAGE_BYTES": "4096", "CBSPMV_DYNAMIC_PAGES": "0"}):
+    os.environ.update(env)
+    for A, opts in reuse:
+        for dt in ("f64", "f32"):
+            tdt = torch.float64 if dt == "f64" else torch.float32
+            h = cb.build(A, dtype=dt, device=0, **opts)
+            x = torch.from_numpy(synth.vector(A.n, 0, 1)).to("cuda:0", tdt)
+            y = torch.empty(A.m, dtype=tdt, device="cuda:0")
+            for _ in range(2):
+                cb.spmv(h, x, y)
+            torch.cuda.synchronize()
+            cb.destroy(h)
+    for k in env:
+        del os.environ[k]
 for A, opts in cases:
     for dt in ("f64", "f32"):
         tdt = torch.float64 if dt == "f64" else torch.float32
