@@ -93,8 +93,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 // Ablation knob for profiling only: built with -DCBSPMV_ABLATION=1 the env CBSPMV_DEBUG_SKIP
-// (a kernel argument) drops the y atomics (bit 0), the x gathers (bit 1) or the item processing
-// (bit 2).  In the production build every test folds away.
+// (a kernel argument) drops the y atomics (bit 0), the x loads (bit 1: x warps' tiles and the
+// COO chunks' gathers) or the item processing (bit 2).  In the production build every test folds away.
 #ifndef CBSPMV_ABLATION
 #define CBSPMV_ABLATION 0
 #endif
@@ -169,7 +169,7 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
 // pg: shared address of the page; da: shared address of the chunk's descriptor
 template <typename M, typename V>
 __device__ __forceinline__ CooPend<V> coo_issue(uint32_t pg, uint32_t da, const V *__restrict__ x, int lane,
-                                                uint64_t pol) {
+                                                uint64_t pol, Dbg dbg) {
   CooPend<V> r;
   const uint4 d = lds_v4(da);
   const int nv = (d.x >> 16) & 0xFF;
@@ -179,7 +179,7 @@ __device__ __forceinline__ CooPend<V> coo_issue(uint32_t pg, uint32_t da, const 
   const uint32_t rbyte = lds_u8(pg + (d.y & 0xFFFFu) + l);
   const uint32_t col = lds_u32(pg + (d.y >> 16) + 4 * l);
   r.v = V(lds_val<M>(pg + (d.z & 0xFFFFu) + (uint32_t)sizeof(M) * l));
-  r.xv = ldg_x(x + col, pol);
+  r.xv = (dbg.skip() & 2) ? V(1) + V(col & 1) : ldg_x(x + col, pol);
   r.row = lds_u32(pg + (d.x & 0xFFFFu) + 4 * (rbyte >> 4)) + (rbyte & 15);
   return r;
 }
@@ -533,18 +533,18 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     for (; k + 3 * W < n; k += 4 * W) {
       CooPend<V> q[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol);
+      for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol, dbg);
       coo_finish<V, SCALED, 4>(q, scale, y, lane, dbg);
     }
     if (k + W < n) {
       CooPend<V> q[2];
 #pragma unroll
-      for (int j = 0; j < 2; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol);
+      for (int j = 0; j < 2; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol, dbg);
       coo_finish<V, SCALED, 2>(q, scale, y, lane, dbg);
       k += 2 * W;
     }
     if (k < n) {
-      CooPend<V> q[1] = {coo_issue<M, V>(pg, dsc + 16u * (uint32_t)k, x, lane, xpol)};
+      CooPend<V> q[1] = {coo_issue<M, V>(pg, dsc + 16u * (uint32_t)k, x, lane, xpol, dbg)};
       coo_finish<V, SCALED, 1>(q, scale, y, lane, dbg);
       k += W;
     }
