@@ -47,10 +47,14 @@ def _reference(A, steps, dtype=torch.float64):
     return x, ss
 
 
-def _simulated_ranks(A, P, steps, dtype="f64"):
-    """P ranks in one process on one GPU, run step-interleaved on one stream."""
+def _simulated_ranks(A, P, steps, dtype="f64", unequal=False):
+    """P ranks in one process on one GPU, run step-interleaved on one stream.  unequal: the
+    shards of dist.shard_bounds (nnz cut at block-row boundaries, unequal row counts)."""
     m_loc = A.m // P
     bounds = [(r * m_loc, (r + 1) * m_loc) for r in range(P)]
+    if unequal:
+        cuts = cbd.shard_bounds(A.row_ptr, P)
+        bounds = cbd.check_row_bounds(list(zip(cuts[:-1], cuts[1:])), A.n)
     hs = [cb.build(cbd.slice_rows(A, a, b), dtype=dtype, device=0) for a, b in bounds]
     xcs = [cb.Exchange(A.n, dtype, P, r, 0) for r in range(P)]
     bases = [xc.base() for xc in xcs]
@@ -96,6 +100,23 @@ def test_fused_exchange_simulated_ranks_match_recurrence(P):
     for x in xs:
         assert np.array_equal(x, xs[0])  # every rank holds the complete, identical iterate
         assert np.allclose(x, x_ref, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("P", [3, 5])
+def test_fused_exchange_unequal_shards(P):
+    """Row shards of different lengths (an nnz cut of a matrix whose rows differ in length):
+    every rank publishes its own slice at its own offset; same recurrence."""
+    _ok()
+    A = synth.make("rmat", small=True)  # power-law rows: the nnz cut gives unequal row counts
+    bounds = cbd.shard_bounds(A.row_ptr, P)
+    assert len(set(np.diff(bounds).tolist())) > 1
+    B = synth.CSR(A.m, A.n, A.row_ptr, A.col, np.abs(A.val))  # nonnegative: a converging iteration
+    steps = 10
+    x_ref, ss_ref = _reference(B, steps)
+    xs, ss = _simulated_ranks(B, P, steps, unequal=True)
+    assert len(set(ss)) == 1 and np.isclose(ss[0], ss_ref, rtol=1e-12)
+    for x in xs:
+        assert np.array_equal(x, xs[0]) and np.allclose(x, x_ref, rtol=1e-11, atol=1e-300)
 
 
 def test_fused_exchange_all_ones_fixed_point():
