@@ -155,7 +155,7 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   const cb::Canon &c = P->canon;
   cb::Stream S;
   CbShape shape;
-  int st = cb_plan_stages(o.device, &shape, err);
+  int st = cb_plan_stages(o.device, c.agg, &shape, err);
   if (st != CBSPMV_OK) return st;
   cb::StreamPlan plan;
   const bool on_device = P->dc != nullptr;  // records on the device: fill the stream there

@@ -253,7 +253,7 @@ struct CbDevice : CbShape {
 
 // Stage shape for a device (env CBSPMV_STAGES / CBSPMV_GROUPS / CBSPMV_GROUP_WARPS /
 // CBSPMV_PAGE_BYTES override the measured defaults; read per build).
-int cb_plan_stages(int device, CbShape *sh, std::string *err);
+int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err);
 // Grid and page assignment for this device and stream (dev's shape already planned).
 int cb_configure(CbDevice *dev, std::string *err);
 // y (+)= A·(s·x); zero_y: clear y first; sumsq: nullptr or device double (s = 1/sqrt(*sumsq)).

@@ -325,7 +325,7 @@ struct KParams {
   int gwarps;  // W consumer warps per group
   int agg;     // aggregated: x gathered by the consumers (restore entries / chunk columns)
   int xvec;    // non-aggregated tiles: x 16-byte aligned -> TMA bulk tile copies
-  int xwarps;  // X x warps (X <= G)
+  int xwarps;  // X x warps (X <= G; 0 for aggregated matrices)
   Dbg dbg;
 };
 
@@ -612,13 +612,16 @@ int env_int(const char *k, int d) {
 // Launch shape, read once per built handle (so a test can build handles with different shapes
 // in one process): S stages, G consumer groups of W warps (G divides S), and the stage bytes
 // that fill the opt-in shared memory.  Defaults measured on B200.
-int cb_plan_stages(int device, CbShape *sh, std::string *err) {
+int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute", err);
-  const int G = std::max(1, env_int("CBSPMV_GROUPS", 4));
-  const int W = std::max(1, env_int("CBSPMV_GROUP_WARPS", 7));
-  const int X = std::max(1, std::min(G, env_int("CBSPMV_XWARPS", 3)));  // X <= G (end markers)
+  // Non-aggregated matrices: 4 groups of 7 warps and 3 x warps (clustered fp64: 0.72 ms; 3 groups
+  // of 9: 0.73, 2 of 14: 0.89).  Aggregated matrices gather x in the consumers, so no x warps:
+  // 2 groups of 15 (R-MAT: 1.05 ms; 4 groups of 7: 1.11, 1 group of 30: 1.08).
+  const int G = std::max(1, env_int("CBSPMV_GROUPS", agg ? 2 : 4));
+  const int W = std::max(1, env_int("CBSPMV_GROUP_WARPS", agg ? 15 : 7));
+  const int X = agg ? 0 : std::max(1, std::min(G, env_int("CBSPMV_XWARPS", 3)));  // X <= G (end markers)
   int S = std::min(kMaxStages, std::max(G, env_int("CBSPMV_STAGES", 12)));
   S -= S % G;  // G | S: every stage belongs to one group
   if (1 + X + G * W > kMaxThreads / 32) {
