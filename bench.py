@@ -426,7 +426,7 @@ def run_power(args, rank, world, local_rank):
     agg = dist.global_agg(A, lambda a: _allreduce_np(a, cdev, world), dtype=args.dtype) if world > 1 else -1
     # column panels: the auto count on one GPU (x slices L2-resident); with N ranks a multiple
     # of N so panel cuts fall on the x owners' boundaries (NEXT-1 (i) overlap)
-    panels = 0 if world == 1 else world * max(1, -(-6 // world))
+    panels = 0 if world == 1 else world * max(1, -(-11 // world))
     h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0, col_panels=panels)
     info = h.info
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
