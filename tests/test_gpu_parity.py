@@ -225,7 +225,14 @@ def decode_stream(stream, page_off):
     return pages
 
 
-@pytest.mark.parametrize("name", ["laplace", "rmat", "clustered"])
+def _member_cap_matrix():
+    """One block row, 40 block columns, one entry per block: COO chunks close at 16 members."""
+    rows = np.arange(40) % 16
+    cols = np.arange(40) * 16 + (np.arange(40) % 5)
+    return synth.from_coo(16, 640, rows, cols, np.linspace(1.0, 2.0, 40), name="member_cap")
+
+
+@pytest.mark.parametrize("name", ["laplace", "rmat", "clustered", "member_cap", "corpus_hub", "corpus_diag"])
 @pytest.mark.parametrize("dtype", ["f64", "f32f64"])
 @pytest.mark.parametrize("device_build", [0, 1])
 def test_device_stream_encodes_canonical_format(name, dtype, device_build):
@@ -235,10 +242,20 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
     original column (restore_cols resolved) and global row.  device_build=1: the stream is filled
     on the device from the device-built records."""
     _ok()
-    A = synth.make(name, small=True)
-    h = cb.build(A, dtype=dtype, device=0, device_build=device_build)
+    if name == "member_cap":
+        A = _member_cap_matrix()
+    elif name == "corpus_hub":
+        A = synth.random_csr(300, 260, 0.08, 17, pattern="hub")
+    elif name == "corpus_diag":
+        A = synth.random_csr(64, 64, 0.05, 3, pattern="diag")
+    else:
+        A = synth.make(name, small=True)
+    opts = {"agg_mode": 0} if name == "member_cap" else {}  # 40 one-entry blocks in one block row
+    h = cb.build(A, dtype=dtype, device=0, device_build=device_build, **opts)
     ex = cb.export(h)
     s, po = cb.download_stream(h)
+    if name == "member_cap":
+        assert ex["nb"] == 40
     pages = decode_stream(s, po)
     S = 8 if dtype == "f64" else 4
     vdt = np.float64 if S == 8 else np.float32
@@ -246,6 +263,7 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
     agg = h.info["agg"]
     mtx, vp = ex["mtx_data"], ex["vp_per_blk"].astype(np.int64)
     nxt = 0
+    shapes = []
     for P in pages:
         pg = P["page"]
         assert P["blk0"] == nxt and P["nblk"] > 0
@@ -303,6 +321,7 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
         for it in chunks:
             nv, nm = it["nv"], it["nm"]
             assert 1 <= nv <= 32 and 1 <= nm <= 16 and it["rb"] % 16 == 0
+            shapes.append((nv, nm))
             rb = pg[it["rb"]:it["rb"] + 4 * nm].view(np.uint32).astype(np.int64)
             assert np.all(rb % 16 == 0)
             rows = pg[it["rows"]:it["rows"] + nv].astype(np.int64)
@@ -319,6 +338,8 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
         # of the page's COO blocks exactly once
         assert sorted(got) == sorted(want)
     assert nxt == ex["nb"]
+    if name == "member_cap":  # the member cap closes chunks before 32 elements
+        assert sorted(shapes) == [(8, 8), (16, 16), (16, 16)]
 
 
 # ----------------------------------------------------------------------------- BASELINE configs
