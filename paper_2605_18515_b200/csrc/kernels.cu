@@ -39,6 +39,7 @@ namespace {
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 32;
 constexpr int kSmemHeader = 1024;  // mbarriers: full[32], xready[32], empty[32]
+constexpr int kAggPageBytes = 20480;  // stage bytes of aggregated matrices (the rest of the array is L1)
 constexpr unsigned kFull = 0xffffffffu;
 // End marker of dynamic page claiming: a 16-byte page header (nitems = kEndItems) copied into
 // the stage by the same TMA path as a page, so the marker is synchronised exactly like data.
@@ -619,10 +620,16 @@ int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err) {
   // Non-aggregated matrices: 4 groups of 7 warps and 3 x warps (clustered fp64: 0.72 ms; 3 groups
   // of 9: 0.73, 2 of 14: 0.89).  Aggregated matrices gather x in the consumers, so no x warps:
   // 2 groups of 15 (R-MAT: 1.05 ms; 4 groups of 7: 1.11, 1 group of 30: 1.08).
+  // Aggregated matrices also leave half the unified L1 / shared array to L1: their x gathers are
+  // random loads whose misses need L1 lines to land in, and with the whole array given to stages
+  // the L1 holds almost nothing (R-MAT 1.10 -> 0.70 ms, uniform 13.1 -> 10.2 ms with 6 stages of
+  // 20 KB: ~120 KB shared, ~100 KB L1; 12 x 19 KB: 1.10 / 13.1, 4 x 24 KB: 0.72, 2 x 32 KB: 1.00).
+  // Non-aggregated matrices stream their x tiles with plain loads and need the deep ring
+  // (clustered: 12 x 19 KB 0.72-0.75 ms, 8 x 19 KB 0.82, 8 x 22 KB 0.78).
   const int G = std::max(1, env_int("CBSPMV_GROUPS", agg ? 2 : 4));
   const int W = std::max(1, env_int("CBSPMV_GROUP_WARPS", agg ? 15 : 7));
   const int X = agg ? 0 : std::max(1, std::min(G, env_int("CBSPMV_XWARPS", 3)));  // X <= G (end markers)
-  int S = std::min(kMaxStages, std::max(G, env_int("CBSPMV_STAGES", 12)));
+  int S = std::min(kMaxStages, std::max(G, env_int("CBSPMV_STAGES", agg ? 6 : 12)));
   S -= S % G;  // G | S: every stage belongs to one group
   if (1 + X + G * W > kMaxThreads / 32) {
     *err = "1 + CBSPMV_XWARPS + CBSPMV_GROUPS * CBSPMV_GROUP_WARPS exceeds 32 warps";
@@ -633,6 +640,7 @@ int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err) {
   probe.gwarps = W;
   int cap = (optin - kSmemHeader - scratch_bytes(probe)) / S / 16 * 16;
   if (const char *v = std::getenv("CBSPMV_PAGE_BYTES")) cap = std::min(cap, std::atoi(v) / 16 * 16);
+  else if (agg) cap = std::min(cap, kAggPageBytes);
   cap = std::min(cap, cb::kMaxPageCap);
   if (cap < 4096) {
     *err = "stage capacity below 4 KB (too many stages for the shared memory)";
