@@ -159,14 +159,21 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   if (st != CBSPMV_OK) return st;
   cb::StreamPlan plan;
   const bool on_device = P->dc != nullptr;  // records on the device: fill the stream there
-  // Chunks whose adjacent elements share a row get the runs flag: the kernel sums each run in the
-  // warp and issues one RED for it.  Power-law hub rows otherwise receive ~10^5 same-address
-  // atomics per SpMV, serialised in L2 (R-MAT: 1.75 -> 1.13 ms).  CBSPMV_COO_RUNS=0 (read per
-  // build) turns the flags off for A/B runs.
-  const char *rv = std::getenv("CBSPMV_COO_RUNS");
-  const bool runs = !(rv && std::atoi(rv) == 0);
+  // Row-run slices (cb_internal.h): a lane sums its piece of a row's run and issues one RED for
+  // it.  Env knobs, read per build, for A/B runs: CBSPMV_RUN_MAX (Lmax, default 8),
+  // CBSPMV_COO_RUNS=0 (Lmax = 1: one RED per element), CBSPMV_RUN_ORDER=row (pieces by row instead
+  // of by length).
+  cb::SliceOpts so;
+  if (const char *v = std::getenv("CBSPMV_RUN_MAX")) so.run_max = std::atoi(v);
+  if (const char *v = std::getenv("CBSPMV_COO_RUNS"); v && std::atoi(v) == 0) so.run_max = 1;
+  if (const char *v = std::getenv("CBSPMV_RUN_ORDER"); v && std::string(v) == "row") so.row_order = 1;
+  cb::CooCoords coords;
+  if (on_device) {  // the records stay on the device: the slice layout needs the COO coordinates
+    st = cb::download_coo_coords(c, *P->dc, cs, &coords, err);
+    if (st != CBSPMV_OK) return st;
+  }
   st = cb::build_stream(c, shape.page_cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err,
-                        runs);
+                        so, on_device ? &coords : nullptr);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   const int64_t npages = (int64_t)S.page_off.size() - 1;
   CbDevice &D = P->dev;

@@ -26,31 +26,35 @@ struct NvtxRange {
 };
 
 // ---------------------------------------------------------------------------
-// Device page stream, version 2.  A derived layout of the canonical format:
+// Device page stream, version 3.  A derived layout of the canonical format:
 // the slot-order blocks (after Alg. 2) are cut into pages of consecutive blocks; one
 // cp.async.bulk moves a page into a shared-memory stage, and the page's x values (gathered by
-// the x warp) follow it in the same stage, so a page is sized by page bytes + x area <= stage.
-//   page = header | item descriptors (16 B each) | item records (16-B aligned)
-//   header: u32 nitems | u32 ncd (CSR / DENSE items; they come first, then the COO chunks)
+// the x warps) follow it in the same stage, so a page is sized by page bytes + x area <= stage.
+//   page = header | item descriptors (16 B each) | slice tables | (pad 16)
+//          | CSR / DENSE records (16-B aligned each) | slice elements
+//   header: u32 nitems | u32 ncd (CSR / DENSE items; they come first, then the COO slices)
 //           | u32 nblk | u32 blk0 (the page's slot-order blocks [blk0, blk0 + nblk))
 // Work items:
 //   * a CSR or DENSE block (the canonical record; DENSE values re-laid lane-major in 16-byte
 //     pairs; with aggregation its restore_cols entries precede the record);
-//   * a COO chunk: up to 32 elements of the page's COO blocks, taken in slot order (a block may
-//     continue into the next chunk), each element with its original column resolved
-//     (restore_cols[cols_offset[br] + bc*16 + c] with aggregation, bc*16 + c without) and a row
-//     byte (member << 4 | local row) indexing the chunk's table of member row bases (<= 16).
-//     chunk record = rowbase u32[nm] | rows u8[nv] (pad 4) | cols u32[nv] (pad to size(Val))
-//                    | vals[nv]; 16-byte aligned.
+//   * a COO slice (row-run slices, a jagged-diagonal layout per page): the elements of the page's
+//     COO blocks, each with its original column resolved (restore_cols[cols_offset[br] + bc*16 + c]
+//     with aggregation, bc*16 + c without), are grouped by global row (a run: the row's elements
+//     in slot order, then canonical (row, col) order); runs longer than Lmax are cut into pieces
+//     of Lmax; the pieces are ordered (length desc, row asc) and dealt 32 to a slice, one per
+//     lane.  Lane l of a slice owns piece l (row rows[l], lens[l] elements); step j holds the
+//     j-th element of every lane whose piece is longer than j, in lane order:
+//       element (l, j) at index off_j + popc(act_j & lanes_below(l)),
+//       act_j = {lanes with lens > j}, off_j = sum_{j' < j} popc(act_j').
+//     slice table = rows u32[nl] | lens u8[nl] (pad 4);  slice elements = cols u32[E] (pad 8)
+//     | vals[E] (pad 8).  The kernel sums a piece in its lane and issues one RED per piece.
 // Item descriptor (uint4 a, b, c, d); d[0,2) type:
 //   CSR / DENSE: a = br*16; b = bc*16 (x tile base) or, aggregated, the page offset of the
 //                restore entries; c = record offset | values offset << 16;
 //                d[2,7) ncols (valid x-tile columns), d[8,16) nnz - 1, d[16,32) x tile offset
 //                in the stage (non-aggregated only: 16 values after the page, filled by TMA)
-//   COO chunk:   a = rowbase offset | nv << 16 | nm << 24; b = rows offset | cols offset << 16;
-//                c = values offset; d[2,5) run steps: ceil(log2(longest run of adjacent
-//                elements sharing a global row)), 0 = no run; the kernel sums each run in the
-//                warp with that many shuffle steps before the RED
+//   COO slice:   a = table offset | nl << 16 | w << 24 (w = longest piece); b = cols offset |
+//                vals offset << 16; c = E (elements); d = 0
 // ---------------------------------------------------------------------------
 #ifdef __CUDACC__
 #define CB_HD __host__ __device__
@@ -59,32 +63,18 @@ struct NvtxRange {
 #endif
 constexpr int kPageHeader = 16;
 constexpr int kDescBytes = 16;
-constexpr int kChunkLanes = 32;
-constexpr int kChunkMembers = 16;          // member index is 4 bits of the row byte
+constexpr int kSliceLanes = 32;
+constexpr int kMaxRun = 255;               // piece length is a u8 (lens[], desc w)
+constexpr int kDefaultRunMax = 8;          // Lmax (env CBSPMV_RUN_MAX, read per build)
 constexpr uint32_t kEndItems = 0xFFFFFFFFu;  // header.nitems of the dynamic-claiming end marker
 constexpr int kMaxPageCap = 65536;         // descriptor offsets are u16 bytes
 constexpr int kCtrSlots = 64;              // page-claim counters per panel (launch k uses slot k % 64)
-constexpr int kRunShift = 2;  // desc.d[2,5): run steps (0..5)
-// steps of a segmented warp sum covering runs of up to maxrun lanes: ceil(log2(maxrun))
-CB_HD inline uint32_t run_steps(int maxrun) {
-  uint32_t s = 0;
-  while ((1 << s) < maxrun) s++;
-  return s;
-}
-
-struct ChunkLayout {
-  int rows, cols, vals, bytes;  // offsets from the chunk record start; total (16-aligned)
-};
-CB_HD inline ChunkLayout chunk_layout(int nv, int nm, int val_size) {
-  ChunkLayout L;
-  L.rows = 4 * nm;
-  L.cols = L.rows + ((nv + 3) & ~3);
-  L.vals = (L.cols + 4 * nv + val_size - 1) / val_size * val_size;
-  L.bytes = (L.vals + val_size * nv + 15) & ~15;
-  return L;
-}
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+// bytes of a slice table (rows u32[nl] | lens u8[nl], 4-aligned) and of its elements (cols u32[E]
+// padded to 8 | vals[E] padded to 8)
+inline int64_t slice_table_bytes(int64_t nl) { return round_up(5 * nl, 4); }
+inline int64_t slice_elem_bytes(int64_t E, int val_size) { return round_up(4 * E, 8) + round_up(val_size * E, 8); }
 
 // Allocator whose value-initialisation is a no-op: resize() of a multi-GB byte buffer leaves the
 // pages untouched, so their first touch happens in the parallel fill threads.
@@ -140,26 +130,35 @@ struct Stream {
   std::vector<uint64_t> page_off;  // n_pages + 1
 };
 // Device-fill plan of the page stream (device builder): the page prefixes (header | item
-// descriptors) in a compact buffer, per slot-order block the stream offset of its record (CSR /
-// DENSE) and restore entries (aggregated), per COO block its first chunk / lane / member, and per
-// chunk its record offset and shape; the records themselves are written on the device.
+// descriptors | slice tables) in a compact buffer, per slot-order block the stream offset of its
+// record (CSR / DENSE; COO: its page) and restore entries (aggregated), per COO block the index of
+// its first element and per COO element its column / value offsets in the page; the records and
+// the slice elements themselves are written on the device.
 struct StreamPlan {
   std::vector<uint8_t> meta;
   std::vector<uint64_t> meta_off;          // n_pages + 1
-  std::vector<uint64_t> rec_dst, res_dst;  // per block: record / restore entries (COO: unused)
+  std::vector<uint64_t> rec_dst, res_dst;  // per block: record (COO: page) / restore entries
   std::vector<int32_t> ncol;               // x-tile columns per block
-  std::vector<int64_t> coo_chunk;          // per block: first chunk (COO), -1 otherwise
-  std::vector<uint8_t> coo_lane, coo_member;
-  std::vector<uint64_t> chunk_off;         // per chunk: stream offset of its record
-  std::vector<uint64_t> chunk_desc;        // per chunk: stream offset of its descriptor
-  std::vector<uint8_t> chunk_nv, chunk_nm;
-  bool runs = true;                        // set the runs flags (fill_stream_device)
+  std::vector<int64_t> coo_e0;             // per block: first element in coo_dst (COO), -1 otherwise
+  std::vector<uint32_t> coo_dst;           // per COO element (slot order, canonical order within
+                                           // its block): col offset | val offset << 16 in the page
+};
+// Coordinate bytes ((col << 4) | row) of the slot-order COO blocks when the records
+// stay on the device (device builder): block i's at bytes[off[i] ..] (off[i] = -1: not COO).
+struct CooCoords {
+  ByteBuf bytes;
+  std::vector<int64_t> off;
+};
+// Row-run slices of the page stream (cb_internal.h layout): Lmax and the piece order.
+struct SliceOpts {
+  int run_max = kDefaultRunMax;  // 1: every element its own piece (no in-lane run sums; A/B)
+  int row_order = 0;             // 0: pieces by (length desc, row asc); 1: by row asc
 };
 // x_size: bytes of one x element (sizes the x area that follows each page in its stage).
 // plan == nullptr: the whole stream is written to host memory (s->bytes); otherwise only the plan.
-// runs = false: no chunk gets the runs flag (A/B of the in-warp run sums).
+// coords: the COO coordinate bytes when c.mtx does not hold the records (nullptr: c.mtx).
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err, bool runs = true);
+                 std::string *err, const SliceOpts &so = SliceOpts(), const CooCoords *coords = nullptr);
 
 // Device-resident canonical arrays kept by the device builder for fill_stream_device.
 struct DevCanon {
@@ -173,6 +172,8 @@ struct DevCanon {
 // (gpu_builder.cu): page prefixes, restore entries, records (DENSE in the lane-major layout).
 int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, const StreamPlan &plan, void *stream,
                        uint8_t *d_stream, std::string *err);
+// The coordinate bytes of the slot-order COO blocks from the device-resident records.
+int download_coo_coords(const Canon &c, const DevCanon &dc, void *stream, CooCoords *out, std::string *err);
 void free_stream(Stream *s);
 
 // Matrix Market coordinate files (mmio.cpp)

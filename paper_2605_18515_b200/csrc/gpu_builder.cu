@@ -521,70 +521,47 @@ __global__ void k_records(int64_t nb, const int32_t *__restrict__ br, const int3
   }
 }
 
-// one warp per COO block: its elements into their chunks (cb_internal.h): element e sits at
-// position lane0 + e of the block's chunk run (chunk c0 + pos / 32, lane pos % 32), member m0 in the
-// first chunk and 0 in the following ones; row byte = member << 4 | local row, the column resolved
-// through restore_cols (aggregated) or bc*16 + local column.
+// one warp per COO block: its elements into their row-run slices (cb_internal.h) at the page
+// offsets the host plan computed (coo_dst: column offset | value offset << 16, page-relative;
+// rec_dst: the block's page), the column resolved through restore_cols (aggregated)
+// or bc*16 + local column.
 template <typename W>
 __global__ void k_coo(int64_t nb, const int32_t *__restrict__ br, const int32_t *__restrict__ bc,
                       const int32_t *__restrict__ nnz, const uint64_t *__restrict__ vp,
-                      const int64_t *__restrict__ chunk, const uint8_t *__restrict__ lane0,
-                      const uint8_t *__restrict__ member0, const uint64_t *__restrict__ chunk_off,
-                      const uint8_t *__restrict__ chunk_nv, const uint8_t *__restrict__ chunk_nm,
-                      const uint8_t *__restrict__ mtx, const uint32_t *__restrict__ restore,
-                      const uint64_t *__restrict__ coff, int agg, uint8_t *__restrict__ stream) {
+                      const int64_t *__restrict__ e0, const uint32_t *__restrict__ dst,
+                      const uint64_t *__restrict__ page, const uint8_t *__restrict__ mtx,
+                      const uint32_t *__restrict__ restore, const uint64_t *__restrict__ coff, int agg,
+                      uint8_t *__restrict__ stream) {
   constexpr int S = (int)sizeof(W);
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (int64_t b = w0; b < nb; b += nw) {
-    const int64_t c0 = chunk[b];
-    if (c0 < 0) continue;
-    const int k = nnz[b], l0 = lane0[b], m0 = member0[b];
+    if (e0[b] < 0) continue;
+    const int k = nnz[b];
     const uint8_t *coord = mtx + vp[b];
     const W *vals = reinterpret_cast<const W *>(coord + k + d_pad(k, S));
-    const uint32_t row0 = (uint32_t)br[b] * kBlk;
     const uint32_t *seg = agg ? restore + coff[br[b]] + (uint64_t)bc[b] * kBlk : nullptr;
-    const int nq = (l0 + k + 31) / 32;
-    if (lane < nq) {  // the block's row base in every chunk it touches
-      const int64_t ch = c0 + lane;
-      reinterpret_cast<uint32_t *>(stream + chunk_off[ch])[lane == 0 ? m0 : 0] = row0;
-    }
+    uint8_t *pg = stream + page[b];
     for (int e = lane; e < k; e += 32) {
-      const int pos = l0 + e, q = pos >> 5, l = pos & 31;
-      const int64_t ch = c0 + q;
-      const ChunkLayout L = chunk_layout(chunk_nv[ch], chunk_nm[ch], S);
-      uint8_t *r = stream + chunk_off[ch];
+      const uint32_t d = dst[e0[b] + e];
       const uint32_t cb = coord[e];  // (col << 4) | row
-      r[L.rows + l] = (uint8_t)(((q ? 0 : m0) << 4) | (cb & 15));
-      reinterpret_cast<uint32_t *>(r + L.cols)[l] = seg ? seg[cb >> 4] : (uint32_t)bc[b] * kBlk + (cb >> 4);
-      reinterpret_cast<W *>(r + L.vals)[l] = vals[e];
+      *reinterpret_cast<uint32_t *>(pg + (d & 0xFFFFu)) = seg ? seg[cb >> 4] : (uint32_t)bc[b] * kBlk + (cb >> 4);
+      *reinterpret_cast<W *>(pg + (d >> 16)) = vals[e];
     }
   }
 }
 
-// one warp per chunk: the run steps (ceil(log2(longest run of adjacent elements sharing a global
-// row))) into its descriptor
-__global__ void k_chunk_flags(int64_t nch, const uint64_t *__restrict__ chunk_off, const uint64_t *__restrict__ chunk_desc,
-                              const uint8_t *__restrict__ chunk_nv, const uint8_t *__restrict__ chunk_nm, int S,
-                              uint8_t *__restrict__ stream) {
+// one warp per COO block: its coordinate bytes into the compact download buffer
+__global__ void k_coo_coords(int64_t nb, const int32_t *__restrict__ nnz, const uint64_t *__restrict__ vp,
+                             const int64_t *__restrict__ coff, const uint8_t *__restrict__ mtx,
+                             uint8_t *__restrict__ out) {
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
-  for (int64_t ch = w0; ch < nch; ch += nw) {
-    const int nv = chunk_nv[ch];
-    const ChunkLayout L = chunk_layout(nv, chunk_nm[ch], S);
-    const uint8_t *r = stream + chunk_off[ch];
-    uint32_t row = 0xFFFFFFFFu - (uint32_t)lane;
-    if (lane < nv) {
-      const uint32_t b = r[L.rows + lane];
-      row = reinterpret_cast<const uint32_t *>(r)[b >> 4] + (b & 15);
-    }
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, row, 1);
-    const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || prev != row);
-    const int head = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // first lane of my run
-    const int maxrun = (int)__reduce_max_sync(0xffffffffu, (unsigned)(lane - head + 1));
-    if (lane == 0) reinterpret_cast<uint32_t *>(stream + chunk_desc[ch])[3] |= run_steps(maxrun) << kRunShift;
+  for (int64_t b = w0; b < nb; b += nw) {
+    if (coff[b] < 0) continue;
+    for (int e = lane; e < nnz[b]; e += 32) out[coff[b] + e] = mtx[vp[b] + e];
   }
 }
 
@@ -602,18 +579,14 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
   const int64_t npages = (int64_t)s.page_off.size() - 1, nb = c.nb;
   if (s.nbytes > 0 && !x.ok(cudaMemsetAsync(d_stream, 0, (size_t)s.nbytes, x.st), "memset stream")) return x.status;
   if (npages <= 0) return x.ok(cudaStreamSynchronize(x.st), "sync") ? CBSPMV_OK : x.status;
-  DBuf d_meta, d_moff, d_poff, d_br, d_bc, d_nnz, d_type, d_vp, d_rdst, d_sdst, d_ncol;
-  DBuf d_cch, d_cl, d_cm, d_coff, d_cnv, d_cnm, d_cdesc;
+  DBuf d_meta, d_moff, d_poff, d_br, d_bc, d_nnz, d_type, d_vp, d_rdst, d_sdst, d_ncol, d_e0, d_dst;
   if (!upload_vec(x, d_meta, plan.meta, "upload plan") || !upload_vec(x, d_moff, plan.meta_off, "upload plan") ||
       !upload_vec(x, d_poff, s.page_off, "upload plan") || !upload_vec(x, d_br, c.br, "upload plan") ||
       !upload_vec(x, d_bc, c.bc, "upload plan") || !upload_vec(x, d_nnz, c.nnzb, "upload plan") ||
       !upload_vec(x, d_type, c.type, "upload plan") || !upload_vec(x, d_vp, c.vp, "upload plan") ||
       !upload_vec(x, d_rdst, plan.rec_dst, "upload plan") || !upload_vec(x, d_ncol, plan.ncol, "upload plan") ||
       (c.agg && !upload_vec(x, d_sdst, plan.res_dst, "upload plan")) ||
-      !upload_vec(x, d_cch, plan.coo_chunk, "upload plan") || !upload_vec(x, d_cl, plan.coo_lane, "upload plan") ||
-      !upload_vec(x, d_cm, plan.coo_member, "upload plan") || !upload_vec(x, d_coff, plan.chunk_off, "upload plan") ||
-      !upload_vec(x, d_cnv, plan.chunk_nv, "upload plan") || !upload_vec(x, d_cnm, plan.chunk_nm, "upload plan") ||
-      !upload_vec(x, d_cdesc, plan.chunk_desc, "upload plan"))
+      !upload_vec(x, d_e0, plan.coo_e0, "upload plan") || !upload_vec(x, d_dst, plan.coo_dst, "upload plan"))
     return x.status;
   k_prefix<<<(int)std::min<int64_t>(npages, 148 * 16), 128, 0, x.st>>>(d_meta.as<uint8_t>(), d_moff.as<uint64_t>(),
                                                                       d_poff.as<uint64_t>(), npages, d_stream);
@@ -625,22 +598,38 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
                                     d_type.as<uint8_t>(), d_vp.as<uint64_t>(), d_rdst.as<uint64_t>(), rd,              \
                                     d_ncol.as<int32_t>(), dc.mtx, dc.restore, dc.cols_offset, d_stream);               \
   k_coo<W><<<g, 256, 0, x.st>>>(nb, d_br.as<int32_t>(), d_bc.as<int32_t>(), d_nnz.as<int32_t>(), d_vp.as<uint64_t>(), \
-                                d_cch.as<int64_t>(), d_cl.as<uint8_t>(), d_cm.as<uint8_t>(), d_coff.as<uint64_t>(),   \
-                                d_cnv.as<uint8_t>(), d_cnm.as<uint8_t>(), dc.mtx, dc.restore, dc.cols_offset, c.agg,  \
-                                d_stream)
+                                d_e0.as<int64_t>(), d_dst.as<uint32_t>(), d_rdst.as<uint64_t>(), dc.mtx, dc.restore,  \
+                                dc.cols_offset, c.agg, d_stream)
     if (c.val_size == 8) {
       CB_FILL(uint64_t);
     } else {
       CB_FILL(uint32_t);
     }
 #undef CB_FILL
-    const int64_t nch = (int64_t)plan.chunk_off.size();
-    if (plan.runs && nch > 0)
-      k_chunk_flags<<<grid_for(nch * 32, 256), 256, 0, x.st>>>(nch, d_coff.as<uint64_t>(), d_cdesc.as<uint64_t>(),
-                                                             d_cnv.as<uint8_t>(), d_cnm.as<uint8_t>(), c.val_size,
-                                                             d_stream);
   }
   if (!x.ok(cudaGetLastError(), "fill launch") || !x.ok(cudaStreamSynchronize(x.st), "sync")) return x.status;
+  return CBSPMV_OK;
+}
+
+int download_coo_coords(const Canon &c, const DevCanon &dc, void *stream, CooCoords *out, std::string *err) {
+  Ctx x{reinterpret_cast<cudaStream_t>(stream), err};
+  const int64_t nb = c.nb;
+  out->off.assign((size_t)nb, -1);
+  int64_t n = 0;
+  for (int64_t i = 0; i < nb; i++)
+    if (c.type[i] == CBSPMV_FMT_COO) { out->off[i] = n; n += c.nnzb[i]; }
+  out->bytes.resize((size_t)n);
+  if (n == 0) return CBSPMV_OK;
+  DBuf d_nnz, d_vp, d_off, d_out;
+  if (!upload_vec(x, d_nnz, c.nnzb, "upload") || !upload_vec(x, d_vp, c.vp, "upload") ||
+      !upload_vec(x, d_off, out->off, "upload") || !x.alloc(d_out, (size_t)n, "alloc"))
+    return x.status;
+  k_coo_coords<<<grid_for(nb * 32, 256), 256, 0, x.st>>>(nb, d_nnz.as<int32_t>(), d_vp.as<uint64_t>(),
+                                                         d_off.as<int64_t>(), dc.mtx, d_out.as<uint8_t>());
+  if (!x.ok(cudaGetLastError(), "coords launch") ||
+      !x.ok(cudaMemcpyAsync(out->bytes.data(), d_out.p, (size_t)n, cudaMemcpyDeviceToHost, x.st), "download") ||
+      !x.ok(cudaStreamSynchronize(x.st), "sync"))
+    return x.status;
   return CBSPMV_OK;
 }
 

@@ -14,10 +14,9 @@
 //       w, w + W, ... counted across its pages (no per-page restart), and arrives on "empty"
 //       after its last item of each page.  y is accumulated with red.global.add — the paper's
 //       atomicAdd:
-//       * COO chunk (Alg. 3): lane <-> element, x[col] gathered into a register
-//         (four chunks' loads in flight per warp); one RED per element issued as one warp
-//         instruction for up to 32 elements; chunks with same-row runs sum them in the warp
-//         first (one RED per run);
+//       * COO slice (Alg. 3, over row-run pieces): lane <-> piece of a row's run,
+//         x[col] gathered into a register (four slices' loads in flight per warp), the piece
+//         summed in the lane, one RED per piece;
 //       * CSR ("32 threads collaboratively compute 16 y elements"): two lanes per
 //         row, one shfl_xor; x tile from the stage (aggregated: gathered through the restore
 //         entries into the warp's scratch);
@@ -129,19 +128,6 @@ __device__ __forceinline__ V ldg_x(const V *p, uint64_t pol) {
   return v;
 }
 
-// COO chunk (Alg. 3): lane <-> element.  Split in two phases so a warp can keep several chunks'
-// loads in flight: coo_issue() reads the lane's row byte, column and value from the page and
-// gathers x[col] into a register (ld.global.nc, L2 evict_last); coo_finish() multiplies and
-// issues the RED (Alg. 3's atomicAdd, one warp instruction for up to 32 elements).  The row byte
-// (member << 4 | local row) indexes the chunk's member row bases.
-template <typename V>
-struct CooPend {
-  V v, xv;         // invalid lanes (>= nv) carry garbage: never summed into a run, never added
-  uint32_t row;
-  uint32_t steps;  // run-sum shuffle steps (0: no run), warp-uniform
-  bool valid;
-};
-
 // 32-bit shared-memory loads (the page lives in the CTA's shared window: no 64-bit generic
 // address arithmetic per element)
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
@@ -167,68 +153,61 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
   return v;
 }
 
-// pg: shared address of the page; da: shared address of the chunk's descriptor
-template <typename M, typename V>
-__device__ __forceinline__ CooPend<V> coo_issue(uint32_t pg, uint32_t da, const V *__restrict__ x, int lane,
-                                                uint64_t pol, Dbg dbg) {
-  CooPend<V> r;
-  const uint4 d = lds_v4(da);
-  const int nv = (d.x >> 16) & 0xFF;
-  r.valid = lane < nv;
-  r.steps = (d.w >> cb::kRunShift) & 7;
-  const uint32_t l = (uint32_t)min(lane, nv - 1);  // invalid lanes re-read the last element
-  const uint32_t rbyte = lds_u8(pg + (d.y & 0xFFFFu) + l);
-  const uint32_t col = lds_u32(pg + (d.y >> 16) + 4 * l);
-  r.v = V(lds_val<M>(pg + (d.z & 0xFFFFu) + (uint32_t)sizeof(M) * l));
-  r.xv = (dbg.skip() & 2) ? V(1) + V(col & 1) : ldg_x(x + col, pol);
-  r.row = lds_u32(pg + (d.x & 0xFFFFu) + 4 * (rbyte >> 4)) + (rbyte & 15);
-  return r;
-}
-
-// Chunks with runs (desc steps > 0, set by the builder: ceil(log2(longest run of adjacent
-// elements sharing a row)) — a COO record is sorted by (row, col)) sum each run in the
-// warp first and the run's first lane issues the one RED; otherwise R-MAT's hub rows receive
-// ~10^5 same-address atomics per SpMV, serialised in L2.  The scan: one ballot of
-// the run ends gives every lane its run's last lane, then `steps` shuffle-adds (a run of up to
-// 2^steps lanes ends up summed on its first lane); a batch of B chunks scans together, so the
-// B shuffle chains overlap.
-template <typename V, bool SCALED, int B>
-__device__ __forceinline__ void coo_finish(const CooPend<V> (&q)[B], V scale, V *__restrict__ y, int lane, Dbg dbg) {
-  V p[B];
-  bool lead[B];
-  uint32_t steps = 0;
+// COO slices (Alg. 3, over row-run pieces; layout in cb_internal.h): lane l owns piece
+// l of the slice — rows[l], lens[l] elements of one row — and walks it step by step: at step j the
+// lanes whose piece is longer than j read their element (index off_j + rank among those lanes),
+// gather x[col] into a register (ld.global.nc, L2 evict_last) and accumulate; then one RED per
+// piece (Alg. 3's atomicAdd).  B slices (items da0, da0 + dstride, ...) advance together so B
+// gathers per lane are in flight.
+template <typename M, typename V, bool SCALED, int B>
+__device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t dstride, const V *__restrict__ x,
+                                           V *__restrict__ y, V scale, int lane, uint64_t pol, Dbg dbg) {
+  uint32_t cv[B], off[B], row[B];  // cv: cols offset | vals offset << 16 (page-relative)
+  int len[B];
+  V acc[B];
+  int wmax = 0;
 #pragma unroll
-  for (int j = 0; j < B; j++) {
-    p[j] = q[j].v * q[j].xv;
-    if constexpr (SCALED) p[j] *= scale;
-    lead[j] = q[j].valid;
-    steps = max(steps, q[j].steps);
+  for (int b = 0; b < B; b++) {
+    const uint4 d = lds_v4(da0 + (uint32_t)b * dstride);
+    const uint32_t nl = (d.x >> 16) & 0xFF, tab = pg + (d.x & 0xFFFFu);
+    const bool in = (uint32_t)lane < nl;
+    len[b] = in ? (int)lds_u8(tab + 4 * nl + lane) : 0;
+    row[b] = in ? lds_u32(tab + 4 * lane) : 0;
+    cv[b] = d.y;
+    off[b] = 0;
+    acc[b] = V(0);
+    wmax = max(wmax, (int)(d.x >> 24));
   }
-  if (steps) {  // warp-uniform: the batch's chunks scan together (B independent shuffle chains)
-    int rem[B];
+  const unsigned below = (1u << lane) - 1u;
+  for (int j = 0; j < wmax; j++) {
+    V xv[B];
+    uint32_t va[B];  // shared address of the lane's value (its load waits until the gathers are issued)
 #pragma unroll
-    for (int j = 0; j < B; j++) {
-      const uint32_t key = q[j].valid ? q[j].row : 0xFFFFFFFFu - (uint32_t)lane;  // invalid lanes: unique keys
-      const uint32_t kn = __shfl_down_sync(kFull, key, 1);
-      const unsigned tails = __ballot_sync(kFull, lane == 31 || kn != key) | 0x80000000u;
-      rem[j] = q[j].steps ? __ffs(tails >> lane) - 1 : 0;  // lanes to the end of my run
-      lead[j] = q[j].valid && (lane == 0 || ((tails >> (lane - 1)) & 1u));  // first lane of its run
-    }
-#pragma unroll
-    for (int s = 0; s < 5; s++) {
-      if (s < (int)steps) {
-        const int d = 1 << s;
-#pragma unroll
-        for (int j = 0; j < B; j++) {
-          const V o = __shfl_down_sync(kFull, p[j], d);
-          if (d <= rem[j]) p[j] += o;
-        }
+    for (int b = 0; b < B; b++) {
+      xv[b] = V(0);
+      va[b] = 0;
+      const bool on = len[b] > j;
+      const unsigned act = __ballot_sync(kFull, on);
+      if (on) {
+        const uint32_t ix = off[b] + (uint32_t)__popc(act & below);
+        const uint32_t c = lds_u32(pg + (cv[b] & 0xFFFFu) + 4u * ix);
+        va[b] = pg + (cv[b] >> 16) + (uint32_t)sizeof(M) * ix;
+        xv[b] = (dbg.skip() & 2) ? V(1) + V(c & 1) : ldg_x(x + c, pol);
       }
+      off[b] += (uint32_t)__popc(act);
     }
+#pragma unroll
+    for (int b = 0; b < B; b++)
+      if (va[b]) acc[b] = fma(V(lds_val<M>(va[b])), xv[b], acc[b]);
   }
 #pragma unroll
-  for (int j = 0; j < B; j++)
-    if (lead[j]) red_add(y + q[j].row, p[j], dbg);
+  for (int b = 0; b < B; b++) {
+    if (len[b] > 0) {
+      V r = acc[b];
+      if constexpr (SCALED) r *= scale;
+      red_add(y + row[b], r, dbg);
+    }
+  }
 }
 
 // Aggregated CSR / DENSE block: its x tile x[restore_cols[cols_offset[br] + bc*16 + c]]
@@ -529,24 +508,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       if ((d.w & 3) == CBSPMV_FMT_CSR) csr_path<M, V, SCALED>(page, d, xt, scale, y, lane, dbg);
       else dense_path<M, V, SCALED>(page, d, xt, scale, y, P.m, lane, dbg);
     }
-    // COO chunks, four at a time: the four chunks' loads and x gathers in flight together
-    const uint32_t pg = smem_addr(page), dsc = pg + cb::kPageHeader;
-    for (; k + 3 * W < n; k += 4 * W) {
-      CooPend<V> q[4];
-#pragma unroll
-      for (int j = 0; j < 4; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol, dbg);
-      coo_finish<V, SCALED, 4>(q, scale, y, lane, dbg);
-    }
+    // COO slices, four at a time: the four slices' element loads and x gathers in flight together
+    const uint32_t pg = smem_addr(page), dsc = pg + cb::kPageHeader, dW = 16u * (uint32_t)W;
+    for (; k + 3 * W < n; k += 4 * W) coo_slices<M, V, SCALED, 4>(pg, dsc + 16u * (uint32_t)k, dW, x, y, scale, lane, xpol, dbg);
     if (k + W < n) {
-      CooPend<V> q[2];
-#pragma unroll
-      for (int j = 0; j < 2; j++) q[j] = coo_issue<M, V>(pg, dsc + 16u * (uint32_t)(k + j * W), x, lane, xpol, dbg);
-      coo_finish<V, SCALED, 2>(q, scale, y, lane, dbg);
+      coo_slices<M, V, SCALED, 2>(pg, dsc + 16u * (uint32_t)k, dW, x, y, scale, lane, xpol, dbg);
       k += 2 * W;
     }
     if (k < n) {
-      CooPend<V> q[1] = {coo_issue<M, V>(pg, dsc + 16u * (uint32_t)k, x, lane, xpol, dbg)};
-      coo_finish<V, SCALED, 1>(q, scale, y, lane, dbg);
+      coo_slices<M, V, SCALED, 1>(pg, dsc + 16u * (uint32_t)k, dW, x, y, scale, lane, xpol, dbg);
       k += W;
     }
     if (n != (int)nitems) k += ((int)nitems - k + W - 1) / W * W;  // ablation skipped the items

@@ -1,12 +1,15 @@
-// stream.cpp — the device page stream (version 2, cb_internal.h / DESIGN.md §4): a derived
+// stream.cpp — the device page stream (version 3, cb_internal.h / DESIGN.md §4): a derived
 // layout of the canonical CB-SpMV format (slot order after Alg. 2) cut into pages that
 // one cp.async.bulk moves into a shared-memory stage.  The paper's intra-block data aggregation
 // (a block's coordinates and values contiguous behind one pointer) is kept per work
 // item: a CSR / DENSE block's canonical record (plus its restore_cols entries) stays one
-// contiguous run; the page's COO blocks are packed lane-contiguously into 32-element chunks with
-// each element's original column resolved, so a warp handles 32 elements with one RED (the
-// paper's warp per COO block leaves >= 50 % of lanes idle).
+// contiguous run.  The page's COO elements (Alg. 3's blocks) are regrouped into
+// row-run slices: each element with its original column resolved (the restore lookup of Alg. 3
+// line 19 done once, here), grouped by global row, pieces of at most Lmax elements dealt one per
+// lane, so a lane sums its piece in a register and issues one RED for it (the paper's warp per COO
+// block leaves >= 50 % of its lanes idle, and issues one atomic per element).
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <vector>
 
@@ -33,89 +36,82 @@ inline int block_ncols(const Canon &c, int64_t i) {
   return (int)std::max<int64_t>(0, std::min<int64_t>(c.blk, w));
 }
 
-// Incremental page state of the greedy page cut (slot order).  COO elements are chunked in
-// order: a chunk closes at 32 elements or when a 17th member (block) would join it.
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// bytes of the slice tables of P pieces (slices of 32 lanes, the last one partial)
+inline int64_t tables_bytes(int64_t P) {
+  if (P == 0) return 0;
+  const int64_t ns = ceil_div(P, kSliceLanes);
+  return (ns - 1) * slice_table_bytes(kSliceLanes) + slice_table_bytes(P - (ns - 1) * kSliceLanes);
+}
+
+// Open-addressing map block row -> slot, reset per page (a page holds at most a few thousand
+// COO blocks); a slot holds the page's element counts of the block row's 16 rows.
+class BrTable {
+ public:
+  BrTable() : key_(kSize, -1), slot_(kSize, 0) {}
+  int find(int32_t br) const {
+    for (uint32_t h = hash(br);; h = (h + 1) & (kSize - 1)) {
+      if (key_[h] == br) return slot_[h];
+      if (key_[h] < 0) return -1;
+    }
+  }
+  int insert(int32_t br) {  // br absent
+    uint32_t h = hash(br);
+    while (key_[h] >= 0) h = (h + 1) & (kSize - 1);
+    key_[h] = br;
+    slot_[h] = (int)cnt_.size();
+    used_.push_back(h);
+    cnt_.emplace_back();
+    cnt_.back().fill(0);
+    return slot_[h];
+  }
+  std::array<int32_t, 16> &counts(int s) { return cnt_[(size_t)s]; }
+  const std::array<int32_t, 16> &counts(int s) const { return cnt_[(size_t)s]; }
+  void clear() {
+    for (uint32_t h : used_) key_[h] = -1;
+    used_.clear();
+    cnt_.clear();
+  }
+  size_t size() const { return used_.size(); }
+
+ private:
+  static constexpr uint32_t kSize = 1u << 15;
+  static uint32_t hash(int32_t br) { return ((uint32_t)br * 2654435761u) >> 17; }
+  std::vector<int32_t> key_;
+  std::vector<int> slot_;
+  std::vector<uint32_t> used_;
+  std::vector<std::array<int32_t, 16>> cnt_;
+};
+
+// Page state of the greedy cut: CSR / DENSE items, COO elements and row-run pieces (exact: the
+// page's per-row element counts are tracked per block row).
 struct PageAcc {
-  int64_t items = 0;         // CSR / DENSE items
-  int64_t rec = 0;           // their record bytes (incl. restore entries, 16-aligned each)
-  int64_t xb = 0;            // their x slots
-  int64_t chunks = 0, chunk_rec = 0;  // closed chunks
-  int nv = 0, nm = 0;        // the open chunk (nv == 0: none)
+  int64_t items = 0;  // CSR / DENSE items
+  int64_t rec = 0;    // their record bytes (incl. restore entries, 16-aligned each)
+  int64_t xb = 0;     // their x slots
+  int64_t E = 0, P = 0;  // COO elements, pieces
+  int64_t blocks = 0;
 };
 
 struct Shape {
-  int val_size, x_size;
+  int val_size, x_size, run_max;
+  // stage bytes of a page in this state: exact but for <= 8 B of element padding per slice
   int64_t stage_bytes(const PageAcc &a) const {
-    const bool open = a.nv > 0;
-    const int64_t items = a.items + a.chunks + (open ? 1 : 0);
-    const int64_t page = round_up(kPageHeader + kDescBytes * items, 16) + a.rec + a.chunk_rec +
-                         (open ? chunk_layout(a.nv, a.nm, val_size).bytes : 0);
-    return page + a.xb;
+    const int64_t ns = ceil_div(a.P, kSliceLanes);
+    const int64_t pre = round_up(kPageHeader + kDescBytes * (a.items + ns) + tables_bytes(a.P), 16);
+    const int64_t el = a.E ? 4 * a.E + val_size * a.E + 8 * ns + 8 : 0;
+    return pre + a.rec + el + a.xb;
   }
-  void close_chunk(PageAcc &a) const {
-    a.chunks++;
-    a.chunk_rec += chunk_layout(a.nv, a.nm, val_size).bytes;
-    a.nv = a.nm = 0;
-  }
-  // append the k elements of one COO block; fn(lane0, member, e0, t) per piece (chunk index =
-  // a.chunks at the call)
-  template <class F>
-  void add_coo(PageAcc &a, int64_t k, F &&fn) const {
-    int64_t e = 0;
-    bool member = false;
-    while (e < k) {
-      if (a.nv == kChunkLanes || (!member && a.nm == kChunkMembers)) {
-        close_chunk(a);
-        member = false;
-      }
-      int m = a.nm - 1;
-      if (!member) { m = a.nm++; member = true; }
-      const int t = (int)std::min<int64_t>(k - e, kChunkLanes - a.nv);
-      fn(a.nv, m, e, t);
-      a.nv += t;
-      e += t;
-      if (e < k) member = false;  // the rest starts the next chunk
-    }
-  }
+  int64_t pieces(int64_t n) const { return ceil_div(n, run_max); }
 };
 
-struct Piece {  // one block's run of elements in one chunk
-  int64_t block, e0, chunk;  // chunk: index within the page
-  int lane0, member, t;
+struct Piece {
+  uint32_t row;
+  int32_t q;     // index of the piece within its row's run
+  int32_t len;
+  int64_t run;   // the run (index into the page's run list)
 };
-
-// The page's COO blocks in the order they are chunked: grouped by block row (stable), so a chunk's
-// elements come from few block rows — fewer 32-byte y sectors per RED and same-row runs across
-// blocks of one block row (R-MAT: 8.2 -> 4.9 sectors per chunk RED, 15.7 -> 11.3 distinct rows).
-// Falls back to slot order when grouping would need more chunk bytes than the page cut (slot
-// order) reserved.  Returns the chunk count; *bytes gets the chunk record bytes.
-int64_t coo_order(const Canon &c, const Shape &sh, int64_t b0, int64_t b1, std::vector<int64_t> &out,
-                  int64_t *bytes) {
-  auto noop = [](int, int, int64_t, int) {};
-  out.clear();
-  for (int64_t i = b0; i < b1; i++)
-    if (c.type[i] == CBSPMV_FMT_COO) out.push_back(i);
-  auto chunk = [&](const std::vector<int64_t> &v, int64_t *b) {
-    PageAcc a;
-    for (int64_t i : v) sh.add_coo(a, c.nnzb[i], noop);
-    if (a.nv) sh.close_chunk(a);
-    *b = a.chunk_rec;
-    return a.chunks;
-  };
-  int64_t slot_bytes = 0;
-  const int64_t slot_chunks = chunk(out, &slot_bytes);
-  std::vector<int64_t> g = out;
-  std::stable_sort(g.begin(), g.end(), [&](int64_t x, int64_t y) { return c.br[x] < c.br[y]; });
-  int64_t g_bytes = 0;
-  const int64_t g_chunks = chunk(g, &g_bytes);
-  if (g_bytes + kDescBytes * g_chunks <= slot_bytes + kDescBytes * slot_chunks) {
-    out.swap(g);
-    *bytes = g_bytes;
-    return g_chunks;
-  }
-  *bytes = slot_bytes;
-  return slot_chunks;
-}
 
 }  // namespace
 
@@ -128,85 +124,138 @@ void free_stream(Stream *s) {
 }
 
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err, bool runs) {
+                 std::string *err, const SliceOpts &so, const CooCoords *coords) {
   if (c.blk != 16) { *err = "the device page stream needs 16x16 blocks"; return CBSPMV_EUNSUPPORTED; }
   if (page_cap > kMaxPageCap || page_cap < 1024) { *err = "stage capacity out of range"; return CBSPMV_EUNSUPPORTED; }
+  if (so.run_max < 1 || so.run_max > kMaxRun) { *err = "run_max out of range [1, 255]"; return CBSPMV_EINVAL; }
   const int T = resolve_threads(threads);
   const int S = c.val_size;
-  const Shape sh{S, x_size};
+  const Shape sh{S, x_size, so.run_max};
   PhaseTimer tm;
+  auto coord = [&](int64_t i) -> const uint8_t * {
+    return coords ? coords->bytes.data() + coords->off[i] : c.mtx.data() + c.vp[i];
+  };
   std::vector<int32_t> ncol((size_t)c.nb);
   std::vector<int64_t> rec((size_t)c.nb);  // CSR / DENSE: device record bytes (restore + record)
-  parallel_for(c.nb, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
+  std::vector<std::array<uint8_t, 16>> rcnt((size_t)c.nb);  // COO: elements per local row
+  parallel_for(c.nb, T, 1 << 14, [&](int64_t lo, int64_t hi, int) {
     for (int64_t i = lo; i < hi; i++) {
       ncol[i] = block_ncols(c, i);
       rec[i] = c.type[i] == CBSPMV_FMT_COO ? 0
                : (c.agg ? round_up(ncol[i], 4) * 4 : 0) + round_up(canon_record_bytes(c, i), 16);
+      if (c.type[i] == CBSPMV_FMT_COO) {
+        rcnt[i].fill(0);
+        const uint8_t *cb = coord(i);
+        for (int e = 0; e < c.nnzb[i]; e++) rcnt[i][cb[e] & 15]++;  // (col << 4) | row
+      }
     }
   });
+  tm.lap("stream: block row counts");
   // ---- greedy page cut: consecutive slot-order blocks while page + x area fits the stage
-  std::vector<int64_t> pb{0};        // first block of each page (+ nb)
-  std::vector<int64_t> page_chunks;  // chunks per page
-  PageAcc cur;
-  auto noop = [](int, int, int64_t, int) {};
-  for (int64_t i = 0; i < c.nb; i++) {
-    PageAcc nx = cur;
-    if (c.type[i] == CBSPMV_FMT_COO) {
-      sh.add_coo(nx, c.nnzb[i], noop);
-    } else {
-      nx.items++; nx.rec += rec[i]; nx.xb += c.agg ? 0 : 16 * (int64_t)x_size;
+  std::vector<int64_t> pb{0};  // first block of each page (+ nb)
+  {
+    PageAcc cur;
+    BrTable tab;
+    for (int64_t i = 0; i < c.nb; i++) {
+      PageAcc nx = cur;
+      int slot = -1;
+      if (c.type[i] == CBSPMV_FMT_COO) {
+        slot = tab.find(c.br[i]);
+        for (int r = 0; r < 16; r++) {
+          const int64_t o = slot >= 0 ? tab.counts(slot)[r] : 0, k = rcnt[i][r];
+          nx.P += sh.pieces(o + k) - sh.pieces(o);
+        }
+        nx.E += c.nnzb[i];
+      } else {
+        nx.items++; nx.rec += rec[i]; nx.xb += c.agg ? 0 : 16 * (int64_t)x_size;
+      }
+      nx.blocks++;
+      if (sh.stage_bytes(nx) <= page_cap) {
+        cur = nx;
+        if (c.type[i] == CBSPMV_FMT_COO) {
+          if (slot < 0) slot = tab.insert(c.br[i]);
+          for (int r = 0; r < 16; r++) tab.counts(slot)[r] += rcnt[i][r];
+        }
+        continue;
+      }
+      if (cur.blocks == 0) { *err = "stage capacity too small for one block"; return CBSPMV_EUNSUPPORTED; }
+      pb.push_back(i);
+      cur = PageAcc{};
+      tab.clear();
+      i--;  // re-add block i to the empty page
     }
-    if (sh.stage_bytes(nx) <= page_cap) { cur = nx; continue; }
-    if (i == pb.back()) { *err = "stage capacity too small for one block"; return CBSPMV_EUNSUPPORTED; }
-    page_chunks.push_back(cur.chunks + (cur.nv > 0));
-    pb.push_back(i);
-    cur = PageAcc{};
-    i--;  // re-add block i to the empty page
+    if (c.nb > pb.back()) pb.push_back(c.nb);
   }
-  if (c.nb > pb.back()) { page_chunks.push_back(cur.chunks + (cur.nv > 0)); pb.push_back(c.nb); }
   const int64_t npages = (int64_t)pb.size() - 1;
-  // page sizes (exact) -> offsets; chunk ids
-  std::vector<uint64_t> off((size_t)npages + 1, 0);
-  std::vector<int64_t> chunk0((size_t)npages + 1, 0);
-  std::vector<int64_t> pbytes((size_t)npages, 0);
-  parallel_for(npages, T, 256, [&](int64_t lo, int64_t hi, int) {
-    std::vector<int64_t> order;
+  tm.lap("stream: page cut");
+
+  // ---- per page: its runs (rows of its COO elements), pieces and slices
+  // Runs are built from the per-row counts (the layout pass) and again from the elements (the fill
+  // pass); both use the same order: rows ascending, a row's elements in slot order then canonical
+  // order, pieces of run_max, then sorted by the piece order.
+  struct Layout {
+    std::vector<uint32_t> rows;  // distinct global rows of the page's COO elements, ascending
+    std::vector<int32_t> cnt;    // elements per row
+    std::vector<Piece> pcs;      // in slice order
+  };
+  auto page_layout = [&](int64_t p, Layout &L) {
+    L.rows.clear(); L.cnt.clear(); L.pcs.clear();
+    std::vector<std::pair<uint32_t, int32_t>> rc;
+    for (int64_t i = pb[p]; i < pb[p + 1]; i++) {
+      if (c.type[i] != CBSPMV_FMT_COO) continue;
+      for (int r = 0; r < 16; r++)
+        if (rcnt[i][r]) rc.emplace_back((uint32_t)c.br[i] * 16u + (uint32_t)r, (int32_t)rcnt[i][r]);
+    }
+    std::sort(rc.begin(), rc.end(), [](const auto &a, const auto &b) { return a.first < b.first; });
+    for (const auto &v : rc) {
+      if (!L.rows.empty() && L.rows.back() == v.first) L.cnt.back() += v.second;
+      else { L.rows.push_back(v.first); L.cnt.push_back(v.second); }
+    }
+    for (int64_t r = 0; r < (int64_t)L.rows.size(); r++)
+      for (int32_t q = 0; q * so.run_max < L.cnt[r]; q++)
+        L.pcs.push_back(Piece{L.rows[r], q, std::min(so.run_max, L.cnt[r] - q * so.run_max), r});
+    if (!so.row_order)  // (length desc, row asc, piece asc); the run list is row-ascending already
+      std::stable_sort(L.pcs.begin(), L.pcs.end(), [](const Piece &a, const Piece &b) { return a.len > b.len; });
+  };
+  auto slice_E = [&](const Layout &L, int64_t s) {
+    int64_t e = 0;
+    const int64_t a = s * kSliceLanes, b = std::min<int64_t>(a + kSliceLanes, (int64_t)L.pcs.size());
+    for (int64_t k = a; k < b; k++) e += L.pcs[k].len;
+    return e;
+  };
+  std::vector<int64_t> pbytes((size_t)npages, 0), pmeta((size_t)npages, 0);
+  parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
+    Layout L;
     for (int64_t p = lo; p < hi; p++) {
-      int64_t items = 0, recb = 0, cbytes = 0;
+      int64_t items = 0, recb = 0;
       for (int64_t i = pb[p]; i < pb[p + 1]; i++)
         if (c.type[i] != CBSPMV_FMT_COO) { items++; recb += rec[i]; }
-      page_chunks[p] = coo_order(c, sh, pb[p], pb[p + 1], order, &cbytes);
-      pbytes[p] = round_up(kPageHeader + kDescBytes * (items + page_chunks[p]), 16) + recb + cbytes;
+      page_layout(p, L);
+      const int64_t Pn = (int64_t)L.pcs.size(), ns = ceil_div(Pn, kSliceLanes);
+      int64_t el = 0;
+      for (int64_t sl = 0; sl < ns; sl++) el += slice_elem_bytes(slice_E(L, sl), S);
+      pmeta[p] = round_up(kPageHeader + kDescBytes * (items + ns) + tables_bytes(Pn), 16);
+      pbytes[p] = round_up(pmeta[p] + recb + el, 16);
     }
   });
-  for (int64_t p = 0; p < npages; p++) {
-    off[p + 1] = off[p] + (uint64_t)pbytes[p];
-    chunk0[p + 1] = chunk0[p] + page_chunks[p];
-  }
-  const int64_t total = (int64_t)off[npages], nchunks = chunk0[npages];
-  tm.lap("stream: page plan");
+  std::vector<uint64_t> off((size_t)npages + 1, 0);
+  for (int64_t p = 0; p < npages; p++) off[p + 1] = off[p] + (uint64_t)pbytes[p];
+  const int64_t total = (int64_t)off[npages];
+  tm.lap("stream: page layout");
   s->nbytes = total;
   s->page_off = off;
   if (plan) {
     plan->meta_off.assign((size_t)npages + 1, 0);
-    for (int64_t p = 0; p < npages; p++) {
-      const int64_t items = (int64_t)page_chunks[p];
-      int64_t n_cd = 0;
-      for (int64_t i = pb[p]; i < pb[p + 1]; i++) n_cd += c.type[i] != CBSPMV_FMT_COO;
-      plan->meta_off[p + 1] = plan->meta_off[p] + (uint64_t)round_up(kPageHeader + kDescBytes * (items + n_cd), 16);
-    }
+    for (int64_t p = 0; p < npages; p++) plan->meta_off[p + 1] = plan->meta_off[p] + (uint64_t)pmeta[p];
     plan->meta.assign((size_t)plan->meta_off[npages], 0);
     plan->rec_dst.assign((size_t)c.nb, 0);
     plan->res_dst.assign(c.agg ? (size_t)c.nb : 0, 0);
     plan->ncol = ncol;
-    plan->coo_chunk.assign((size_t)c.nb, -1);
-    plan->coo_lane.assign((size_t)c.nb, 0);
-    plan->coo_member.assign((size_t)c.nb, 0);
-    plan->chunk_off.assign((size_t)nchunks, 0);
-    plan->chunk_desc.assign((size_t)nchunks, 0);
-    plan->runs = runs;
-    plan->chunk_nv.assign((size_t)nchunks, 0);
-    plan->chunk_nm.assign((size_t)nchunks, 0);
+    plan->coo_e0.assign((size_t)c.nb, -1);
+    int64_t ne = 0;
+    for (int64_t i = 0; i < c.nb; i++)
+      if (c.type[i] == CBSPMV_FMT_COO) { plan->coo_e0[i] = ne; ne += c.nnzb[i]; }
+    plan->coo_dst.assign((size_t)ne, 0);
   } else if (total > 0) {
     void *p = nullptr;
     // Pageable by default: pinning a multi-GB buffer costs more (measured 2.7 s for the 4.2 GB
@@ -225,41 +274,41 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
   tm.lap(plan ? "stream: device plan alloc" : s->pinned ? "stream: pinned alloc" : "stream: pageable alloc");
 
   // ---- fill: one page at a time
+  struct Elem {
+    uint32_t row;
+    int64_t blk;
+    int32_t e;  // index within the block's canonical record
+  };
   parallel_for(npages, T, 64, [&](int64_t lo, int64_t hi, int) {
-    std::vector<Piece> pieces;
-    std::vector<int> cnv, cnm;           // per chunk of the page
-    std::vector<int64_t> cd;              // CSR / DENSE blocks of the page
-    std::vector<int64_t> order;           // its COO blocks in chunk order
+    Layout L;
+    std::vector<int64_t> cd;                 // CSR / DENSE blocks of the page
+    std::vector<Elem> el;                    // the page's COO elements
+    std::vector<int64_t> run0;               // per run: its first element in el (sorted by row)
+    std::vector<int32_t> idx;                // per slice: element index of (lane, step)
     for (int64_t p = lo; p < hi; p++) {
-      pieces.clear(); cnv.clear(); cnm.clear(); cd.clear();
-      PageAcc a;
-      for (int64_t i = pb[p]; i < pb[p + 1]; i++)
-        if (c.type[i] != CBSPMV_FMT_COO) cd.push_back(i);
-      int64_t cbytes = 0;
-      coo_order(c, sh, pb[p], pb[p + 1], order, &cbytes);
-      for (int64_t i : order) {
-        // at each call a.chunks is the index of the chunk the piece lands in (add_coo closes first)
-        sh.add_coo(a, c.nnzb[i], [&](int lane0, int member, int64_t e0, int t) {
-          pieces.push_back(Piece{i, e0, a.chunks, lane0, member, t});
-        });
+      cd.clear(); el.clear();
+      for (int64_t i = pb[p]; i < pb[p + 1]; i++) {
+        if (c.type[i] != CBSPMV_FMT_COO) { cd.push_back(i); continue; }
+        const uint8_t *cb = coord(i);
+        for (int e = 0; e < c.nnzb[i]; e++) el.push_back(Elem{(uint32_t)c.br[i] * 16u + (cb[e] & 15u), i, e});
       }
-      if (a.nv) sh.close_chunk(a);
-      cnv.assign((size_t)a.chunks, 0);
-      cnm.assign((size_t)a.chunks, 0);
-      for (const Piece &pc : pieces) {
-        const size_t ch = (size_t)pc.chunk;
-        const int t = pc.t;
-        cnv[ch] = std::max(cnv[ch], pc.lane0 + t);
-        cnm[ch] = std::max(cnm[ch], pc.member + 1);
-      }
-      const int64_t nch = (int64_t)cnv.size();
-      const int64_t nitems = (int64_t)cd.size() + nch;
+      // rows ascending; a row's elements in slot order, then canonical order (stable)
+      std::stable_sort(el.begin(), el.end(), [](const Elem &a, const Elem &b) { return a.row < b.row; });
+      page_layout(p, L);
+      const int64_t nruns = (int64_t)L.rows.size(), Pn = (int64_t)L.pcs.size();
+      const int64_t ns = ceil_div(Pn, kSliceLanes);
+      run0.assign((size_t)nruns + 1, 0);
+      for (int64_t r = 0; r < nruns; r++) run0[r + 1] = run0[r] + L.cnt[r];
+
+      const int64_t nitems = (int64_t)cd.size() + ns;
       const int64_t desc0 = kPageHeader;
-      int64_t pos = round_up(kPageHeader + kDescBytes * nitems, 16);
+      int64_t tpos = kPageHeader + kDescBytes * nitems;  // slice tables
+      int64_t pos = pmeta[p];                            // records, then slice elements
       const int64_t xoff = pbytes[p];
       int64_t xpos = xoff;
       uint8_t *page = plan ? plan->meta.data() + plan->meta_off[p] : s->bytes + off[p];
-      if (!plan) std::memset(page, 0, (size_t)pbytes[p]);
+      const int64_t wbytes = plan ? pmeta[p] : pbytes[p];  // bytes of `page` written here
+      std::memset(page, 0, (size_t)wbytes);
       const uint32_t hdr[4] = {(uint32_t)nitems, (uint32_t)cd.size(), (uint32_t)(pb[p + 1] - pb[p]), (uint32_t)pb[p]};
       std::memcpy(page, hdr, 16);
       int64_t it = 0;
@@ -269,8 +318,8 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
         const int64_t res = c.agg ? pos : 0;
         if (c.agg) pos += round_up(ncol[i], 4) * 4;
         const int64_t body = pos;
-        const int64_t idx = type == CBSPMV_FMT_CSR ? (c.blk + 1) + k : 0;
-        const int64_t vals = body + round_up(idx, S);
+        const int64_t idxb = type == CBSPMV_FMT_CSR ? (c.blk + 1) + k : 0;
+        const int64_t vals = body + round_up(idxb, S);
         uint32_t d[4];
         d[0] = (uint32_t)c.br[i] * (uint32_t)c.blk;
         d[1] = c.agg ? (uint32_t)res : (uint32_t)c.bc[i] * (uint32_t)c.blk;
@@ -303,74 +352,62 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
         }
         pos = body + round_up(canon_record_bytes(c, i), 16);
       }
-      // COO chunks
-      std::vector<int64_t> crec((size_t)nch);
-      for (int64_t ch = 0; ch < nch; ch++) {
-        const ChunkLayout L = chunk_layout(cnv[ch], cnm[ch], S);
-        crec[ch] = pos;
+      // COO slices: descriptors, tables (in the prefix) and elements (after the records)
+      std::vector<int64_t> cols_at((size_t)ns), vals_at((size_t)ns);
+      std::vector<int32_t> w_of((size_t)ns);
+      for (int64_t sl = 0; sl < ns; sl++) {
+        const int64_t a = sl * kSliceLanes, nl = std::min<int64_t>(kSliceLanes, Pn - a);
+        int w = 0;
+        for (int64_t l = 0; l < nl; l++) {
+          const Piece &pc = L.pcs[a + l];
+          std::memcpy(page + tpos + 4 * l, &pc.row, 4);
+          page[tpos + 4 * nl + l] = (uint8_t)pc.len;
+          w = std::max(w, pc.len);
+        }
+        const int64_t E = slice_E(L, sl);
+        cols_at[sl] = pos;
+        vals_at[sl] = pos + round_up(4 * E, 8);
+        w_of[sl] = w;
         uint32_t d[4];
-        d[0] = (uint32_t)pos | ((uint32_t)cnv[ch] << 16) | ((uint32_t)cnm[ch] << 24);
-        d[1] = (uint32_t)(pos + L.rows) | ((uint32_t)(pos + L.cols) << 16);
-        d[2] = (uint32_t)(pos + L.vals);
-        d[3] = (uint32_t)CBSPMV_FMT_COO;  // the runs flag is set once the elements are in place
+        d[0] = (uint32_t)tpos | ((uint32_t)nl << 16) | ((uint32_t)w << 24);
+        d[1] = (uint32_t)cols_at[sl] | ((uint32_t)vals_at[sl] << 16);
+        d[2] = (uint32_t)E;
+        d[3] = (uint32_t)CBSPMV_FMT_COO;
         std::memcpy(page + desc0 + kDescBytes * it, d, 16);
         it++;
-        if (plan) {
-          plan->chunk_off[chunk0[p] + ch] = off[p] + (uint64_t)pos;
-          plan->chunk_desc[chunk0[p] + ch] = off[p] + (uint64_t)(desc0 + kDescBytes * (it - 1));
-          plan->chunk_nv[chunk0[p] + ch] = (uint8_t)cnv[ch];
-          plan->chunk_nm[chunk0[p] + ch] = (uint8_t)cnm[ch];
-        }
-        pos += L.bytes;
+        tpos += slice_table_bytes(nl);
+        pos += slice_elem_bytes(E, S);
       }
-      for (const Piece &pc : pieces) {
-        const int64_t ch = pc.chunk;
-        const int t = pc.t;
-        const int64_t i = pc.block;
-        if (plan) {
-          if (pc.e0 == 0) {
-            plan->coo_chunk[i] = chunk0[p] + ch;
-            plan->coo_lane[i] = (uint8_t)pc.lane0;
-            plan->coo_member[i] = (uint8_t)pc.member;
+      // element (lane l, step j) of a slice sits at off_j + (lanes below l whose piece is longer than j)
+      for (int64_t sl = 0; sl < ns; sl++) {
+        const int64_t a = sl * kSliceLanes, nl = std::min<int64_t>(kSliceLanes, Pn - a);
+        const int w = w_of[sl];
+        idx.assign((size_t)kSliceLanes * w, -1);
+        int32_t o = 0;
+        for (int j = 0; j < w; j++)
+          for (int64_t l = 0; l < nl; l++)
+            if (L.pcs[a + l].len > j) idx[(size_t)l * w + j] = o++;
+        // place this slice's elements
+        for (int64_t l = 0; l < nl; l++) {
+          const Piece &pc = L.pcs[a + l];
+          const int64_t e0 = run0[pc.run] + (int64_t)pc.q * so.run_max;
+          for (int j = 0; j < pc.len; j++) {
+            const Elem &E = el[(size_t)(e0 + j)];
+            const int64_t ix = idx[(size_t)l * w + j];
+            const uint32_t co = (uint32_t)(cols_at[sl] + 4 * ix), vo = (uint32_t)(vals_at[sl] + S * ix);
+            const int64_t i = E.blk;
+            if (plan) {
+              plan->coo_dst[(size_t)(plan->coo_e0[i] + E.e)] = co | (vo << 16);
+              plan->rec_dst[i] = off[p];
+              continue;
+            }
+            const int64_t k = c.nnzb[i];
+            const uint8_t b = coord(i)[E.e];  // (col << 4) | row
+            const uint32_t col = c.agg ? c.restore[c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk + (b >> 4)]
+                                       : (uint32_t)c.bc[i] * (uint32_t)c.blk + (b >> 4);
+            std::memcpy(page + co, &col, 4);
+            std::memcpy(page + vo, c.mtx.data() + c.vp[i] + round_up(k, S) + (int64_t)S * E.e, (size_t)S);
           }
-          continue;
-        }
-        const ChunkLayout L = chunk_layout(cnv[ch], cnm[ch], S);
-        uint8_t *r = page + crec[ch];
-        const uint32_t row0 = (uint32_t)c.br[i] * (uint32_t)c.blk;
-        std::memcpy(r + 4 * pc.member, &row0, 4);
-        const int64_t k = c.nnzb[i];
-        const uint8_t *coord = c.mtx.data() + c.vp[i];
-        const uint8_t *vals = coord + round_up(k, S);
-        const uint32_t *seg = c.agg ? c.restore.data() + c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk : nullptr;
-        for (int j = 0; j < t; j++) {
-          const int64_t e = pc.e0 + j;
-          const int lane = pc.lane0 + j;
-          const uint8_t b = coord[e];  // (col << 4) | row
-          r[L.rows + lane] = (uint8_t)((pc.member << 4) | (b & 15));
-          const uint32_t col = seg ? seg[b >> 4] : (uint32_t)c.bc[i] * (uint32_t)c.blk + (b >> 4);
-          std::memcpy(r + L.cols + 4 * lane, &col, 4);
-          std::memcpy(r + L.vals + (int64_t)S * lane, vals + e * S, (size_t)S);
-        }
-      }
-      // run steps: the longest run of adjacent elements sharing a global row (a COO record is
-      // sorted by (row, col), so a row's elements in one block are adjacent)
-      if (!plan && runs) {
-        for (int64_t ch = 0; ch < nch; ch++) {
-          const ChunkLayout L = chunk_layout(cnv[ch], cnm[ch], S);
-          const uint8_t *r = page + crec[ch];
-          uint32_t prev = 0xFFFFFFFFu;
-          int len = 0, maxrun = 1;
-          for (int l = 0; l < cnv[ch]; l++) {
-            uint32_t rb;
-            std::memcpy(&rb, r + 4 * (r[L.rows + l] >> 4), 4);
-            const uint32_t row = rb + (r[L.rows + l] & 15);
-            len = row == prev ? len + 1 : 1;
-            maxrun = std::max(maxrun, len);
-            prev = row;
-          }
-          uint32_t *dw = reinterpret_cast<uint32_t *>(page + desc0 + kDescBytes * ((int64_t)cd.size() + ch)) + 3;
-          *dw |= run_steps(maxrun) << kRunShift;
         }
       }
     }

@@ -170,11 +170,12 @@ def test_exact_integer_bitwise_device_built(pattern):
 
 
 @pytest.mark.parametrize("A", CORPUS[::3], ids=lambda A: A.name)
-def test_device_built_with_run_sums_forced(A, monkeypatch):
-    """The chunk runs flags (set on the device by k_chunk_flags) and the run sums on device-built
-    handles; the stream-decode test checks the flags themselves."""
+@pytest.mark.parametrize("run_max", ["1", "3", "32"])
+def test_device_built_coo_slices(A, run_max, monkeypatch):
+    """Row-run slices filled on the device (k_coo at the host plan's offsets) on device-built
+    handles, for several Lmax; the stream-decode test checks the layout itself."""
     _ok()
-    monkeypatch.setenv("CBSPMV_COO_RUNS", "1")
+    monkeypatch.setenv("CBSPMV_RUN_MAX", run_max)
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=12)
     y_ref, R = oracle.spmv_csr(A, x)
     for agg in (0, 1):

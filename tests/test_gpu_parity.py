@@ -204,8 +204,8 @@ def test_dense_block_in_partial_last_block_row():
 
 # ----------------------------------------------------------------------------- device layout
 def decode_stream(stream, page_off):
-    """Decode the device page stream, version 2 (cb_internal.h): per page its header,
-    item descriptors, CSR / DENSE records and COO chunk elements."""
+    """Decode the device page stream, version 3 (cb_internal.h): per page its header,
+    item descriptors, CSR / DENSE records and COO row-run slices."""
     pages = []
     for p in range(len(page_off) - 1):
         pg = stream[int(page_off[p]):int(page_off[p + 1])]
@@ -215,9 +215,8 @@ def decode_stream(stream, page_off):
         for a, b, c, d in (tuple(int(v) for v in row) for row in desc):
             t, xslot = d & 3, d >> 16
             if t == 0:
-                nv, nm = (a >> 16) & 0xFF, a >> 24
-                items.append(dict(type=0, rb=a & 0xFFFF, nv=nv, nm=nm, rows=b & 0xFFFF, cols=b >> 16,
-                                  vals=c & 0xFFFF, steps=(d >> 2) & 7, xslot=xslot))
+                items.append(dict(type=0, tab=a & 0xFFFF, nl=(a >> 16) & 0xFF, w=a >> 24, cols=b & 0xFFFF,
+                                  vals=b >> 16, E=c, d=d))
             else:
                 items.append(dict(type=t, row0=a, xinfo=b, body=c & 0xFFFF, vals=c >> 16, ncols=(d >> 2) & 31,
                                   nnz=((d >> 8) & 0xFF) + 1, xslot=xslot))
@@ -225,36 +224,73 @@ def decode_stream(stream, page_off):
     return pages
 
 
-def _member_cap_matrix():
-    """One block row, 40 block columns, one entry per block: COO chunks close at 16 members."""
+def decode_slice(pg, it, S, vdt):
+    """One COO slice: its pieces (row, length) and, per piece, its elements (column, value) in step
+    order -- element (lane l, step j) at off_j + (lanes below l whose piece is longer than j)."""
+    nl = it["nl"]
+    rows = pg[it["tab"]:it["tab"] + 4 * nl].view(np.uint32).astype(np.int64)
+    lens = pg[it["tab"] + 4 * nl:it["tab"] + 5 * nl].astype(np.int64)
+    E = int(lens.sum())
+    cols = pg[it["cols"]:it["cols"] + 4 * E].view(np.uint32).astype(np.int64)
+    vals = pg[it["vals"]:it["vals"] + S * E].view(vdt)
+    elems = [[] for _ in range(nl)]
+    off = 0
+    for j in range(int(lens.max()) if nl else 0):
+        act = np.flatnonzero(lens > j)
+        for r, l in enumerate(act):
+            elems[l].append((int(cols[off + r]), float(vals[off + r])))
+        off += len(act)
+    return rows, lens, elems
+
+
+def _one_block_row_matrix():
+    """One block row, 40 block columns, one entry per block: 16 rows with runs of 2 or 3."""
     rows = np.arange(40) % 16
     cols = np.arange(40) * 16 + (np.arange(40) % 5)
-    return synth.from_coo(16, 640, rows, cols, np.linspace(1.0, 2.0, 40), name="member_cap")
+    return synth.from_coo(16, 640, rows, cols, np.linspace(1.0, 2.0, 40), name="one_block_row")
 
 
-@pytest.mark.parametrize("name", ["laplace", "rmat", "clustered", "member_cap", "corpus_hub", "corpus_diag"])
+def _long_run_matrix():
+    """Row 3 holds 200 entries, one per block column (200 one-entry COO blocks of block row 0):
+    one run of 200 elements, cut into pieces of Lmax."""
+    cols = np.arange(200) * 16 + 7
+    return synth.from_coo(16, 3200, np.full(200, 3), cols, np.linspace(-1.0, 1.0, 200), name="long_run")
+
+
+@pytest.mark.parametrize("name", ["laplace", "rmat", "clustered", "one_block_row", "long_run", "corpus_hub",
+                                  "corpus_diag"])
 @pytest.mark.parametrize("dtype", ["f64", "f32f64"])
 @pytest.mark.parametrize("device_build", [0, 1])
-def test_device_stream_encodes_canonical_format(name, dtype, device_build):
+@pytest.mark.parametrize("runopt", ["", "RUN_MAX=7", "RUN_MAX=32", "RUN_ORDER=row"])
+def test_device_stream_encodes_canonical_format(name, dtype, device_build, runopt, monkeypatch):
     """What is on the device is exactly the canonical format (slot order): pages tile the slot
     order; CSR / DENSE records byte-equal (DENSE re-laid lane-major), their restore entries equal
-    restore_cols; the COO chunks hold exactly the page's COO elements in slot order, each with its
-    original column (restore_cols resolved) and global row.  device_build=1: the stream is filled
-    on the device from the device-built records."""
+    restore_cols; the COO slices hold exactly the page's COO elements, each with its original
+    column (restore_cols resolved), grouped into row runs (a row's elements in slot order, then
+    canonical order), cut into pieces of Lmax, ordered (length desc, row asc) or by row, 32 pieces
+    per slice.  device_build=1: the stream is filled on the device from the device-built records."""
     _ok()
-    if name == "member_cap":
-        A = _member_cap_matrix()
+    run_max = 8  # kDefaultRunMax
+    if runopt:
+        k, v = runopt.split("=")
+        monkeypatch.setenv("CBSPMV_" + k, v)
+        run_max = int(v) if k == "RUN_MAX" else run_max
+    row_order = runopt == "RUN_ORDER=row"
+    if name == "one_block_row":
+        A = _one_block_row_matrix()
+    elif name == "long_run":
+        A = _long_run_matrix()
     elif name == "corpus_hub":
         A = synth.random_csr(300, 260, 0.08, 17, pattern="hub")
     elif name == "corpus_diag":
         A = synth.random_csr(64, 64, 0.05, 3, pattern="diag")
     else:
         A = synth.make(name, small=True)
-    opts = {"agg_mode": 0} if name == "member_cap" else {}  # 40 one-entry blocks in one block row
+    opts = {"agg_mode": 0} if name in ("one_block_row", "long_run") else {}  # one-entry blocks stay apart
     h = cb.build(A, dtype=dtype, device=0, device_build=device_build, **opts)
     ex = cb.export(h)
     s, po = cb.download_stream(h)
-    if name == "member_cap":
+    if name == "one_block_row":
         assert ex["nb"] == 40
     pages = decode_stream(s, po)
     S = 8 if dtype == "f64" else 4
@@ -272,8 +308,8 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
         assert len(pg) % 16 == 0
         cd = [i for i in blocks if ex["type_per_blk"][i] != 0]
         items_cd = [it for it in P["items"] if it["type"] != 0]
-        chunks = [it for it in P["items"] if it["type"] == 0]
-        assert [it["type"] for it in P["items"]] == [1 if ex["type_per_blk"][i] == 1 else 2 for i in cd] + [0] * len(chunks)
+        slices = [it for it in P["items"] if it["type"] == 0]
+        assert [it["type"] for it in P["items"]] == [1 if ex["type_per_blk"][i] == 1 else 2 for i in cd] + [0] * len(slices)
         assert P["ncd"] == len(cd)
         # x tiles (non-aggregated CSR / DENSE only): 16 values each, consecutive after the page
         end = len(pg)
@@ -281,7 +317,7 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
             if it["type"] and not agg:
                 assert it["xslot"] == end
                 end += 16 * xs
-            else:
+            elif it["type"]:
                 assert it["xslot"] == 0
         for i, it in zip(cd, items_cd):
             br, bc, nnz, typ = (int(ex[k][i]) for k in ("blk_row_idx", "blk_col_idx", "nnz_per_blk", "type_per_blk"))
@@ -306,8 +342,8 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
                 src = (l % 16) * 16 + (l // 16) * 8 + 2 * q + hh
                 dev_rec = dev_rec.view(vdt)[np.argsort(src)].view(np.uint8)
             assert np.array_equal(dev_rec, mtx[vp[i]:vp[i] + size])
-        # COO elements of the page in slot order: (global row, original column, value bytes)
-        want = []
+        # the page's COO elements per row, in slot order then canonical order: (original column, value)
+        want = {}
         for i in blocks:
             if ex["type_per_blk"][i] != 0:
                 continue
@@ -316,30 +352,34 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build):
             vals = mtx[vp[i] + k + (-k) % S:vp[i] + k + (-k) % S + k * S].view(vdt)
             cols = (ex["restore_cols"][int(ex["cols_offset"][br]) + 16 * bc + (coord >> 4)].astype(np.int64) if agg
                     else 16 * bc + (coord >> 4))
-            want += list(zip((16 * br + (coord & 15)).tolist(), cols.tolist(), vals.tolist()))
-        got = []
-        for it in chunks:
-            nv, nm = it["nv"], it["nm"]
-            assert 1 <= nv <= 32 and 1 <= nm <= 16 and it["rb"] % 16 == 0
-            shapes.append((nv, nm))
-            rb = pg[it["rb"]:it["rb"] + 4 * nm].view(np.uint32).astype(np.int64)
-            assert np.all(rb % 16 == 0)
-            rows = pg[it["rows"]:it["rows"] + nv].astype(np.int64)
-            assert np.all((rows >> 4) < nm)
-            cols = pg[it["cols"]:it["cols"] + 4 * nv].view(np.uint32).astype(np.int64)
-            vals = pg[it["vals"]:it["vals"] + S * nv].view(vdt)
-            g = rb[rows >> 4] + (rows & 15)
-            # run steps: ceil(log2(longest run of adjacent elements sharing a row))
-            brk = np.flatnonzero(np.diff(g) != 0)
-            maxrun = int(np.max(np.diff(np.concatenate([[-1], brk, [len(g) - 1]]))))
-            assert it["steps"] == int(np.ceil(np.log2(maxrun))) if maxrun > 1 else it["steps"] == 0
-            got += list(zip(g.tolist(), cols.tolist(), vals.tolist()))
-        # the page's COO blocks are chunked grouped by block row (or in slot order): every element
-        # of the page's COO blocks exactly once
+            for r, c_, v in zip((16 * br + (coord & 15)).tolist(), cols.tolist(), vals.tolist()):
+                want.setdefault(r, []).append((c_, v))
+        pieces, got = [], {}
+        tab = 16 + 16 * P["nitems"]
+        for n_s, it in enumerate(slices):
+            assert it["d"] == 0 and it["tab"] == tab
+            rows, lens, elems = decode_slice(pg, it, S, vdt)
+            tab += (5 * it["nl"] + 3) // 4 * 4
+            assert 1 <= it["nl"] <= 32 and (it["nl"] == 32 or n_s == len(slices) - 1)
+            assert np.all(lens >= 1) and np.all(lens <= run_max)
+            assert it["w"] == lens.max() and it["E"] == lens.sum()
+            assert it["vals"] == it["cols"] + (4 * it["E"] + 7) // 8 * 8
+            shapes.append((it["nl"], it["w"]))
+            for r, ln, el in zip(rows.tolist(), lens.tolist(), elems):
+                pieces.append((r, ln))
+                got.setdefault(r, []).append(el)
+        # pieces: a row's run cut into pieces of Lmax (the last shorter), in the piece order
+        key = (lambda pc: pc[0]) if row_order else (lambda pc: (-pc[1], pc[0]))
+        assert pieces == sorted(pieces, key=key)
         assert sorted(got) == sorted(want)
+        for r, run in want.items():
+            assert [len(e) for e in got[r]] == [min(run_max, len(run) - q) for q in range(0, len(run), run_max)]
+            assert [e for piece in got[r] for e in piece] == run
     assert nxt == ex["nb"]
-    if name == "member_cap":  # the member cap closes chunks before 32 elements
-        assert sorted(shapes) == [(8, 8), (16, 16), (16, 16)]
+    if name == "one_block_row":  # rows 0-7 hold 3 entries, 8-15 hold 2: one slice of 16 pieces
+        assert shapes == [(16, 3)] if run_max >= 3 else True
+    if name == "long_run" and not row_order:
+        assert sum(nl for nl, _ in shapes) == -(-200 // run_max)
 
 
 # ----------------------------------------------------------------------------- BASELINE configs
@@ -602,13 +642,19 @@ def test_spmv_host_batch_pipelined(count, dtype):
     cb.destroy(h)
 
 
+_RUNOPTS = [{"CBSPMV_COO_RUNS": "0"}, {"CBSPMV_RUN_MAX": "1"}, {"CBSPMV_RUN_MAX": "2"}, {"CBSPMV_RUN_MAX": "5"},
+            {}, {"CBSPMV_RUN_MAX": "32"}, {"CBSPMV_RUN_MAX": "255"}, {"CBSPMV_RUN_ORDER": "row"}, {"CBSPMV_RUN_ORDER": "row", "CBSPMV_RUN_MAX": "3"}]
+_runid = lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()) or "default"
+
+
 @pytest.mark.parametrize("A", CORPUS[::2], ids=lambda A: A.name)
 @pytest.mark.parametrize("dtype", ["f64", "f32", "f32f64"])
-@pytest.mark.parametrize("runs", ["0", "1"])
-def test_coo_run_sums_on_and_off(A, dtype, runs, monkeypatch):
-    """The in-warp sums of same-row runs of a COO chunk before the RED (chunks flagged by the
-    builder), and the same path with every flag off."""
-    monkeypatch.setenv("CBSPMV_COO_RUNS", runs)
+@pytest.mark.parametrize("runopt", _RUNOPTS, ids=_runid)
+def test_coo_slice_options(A, dtype, runopt, monkeypatch):
+    """COO row-run slices under every build option: Lmax (1 = one RED per element), the piece
+    order (length desc / row), CBSPMV_COO_RUNS=0 (= Lmax 1)."""
+    for k, v in runopt.items():
+        monkeypatch.setenv(k, v)
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=5)
     for agg in (0, 1):
         y, h = gpu_spmv(A, x, dtype=dtype, agg_mode=agg)
@@ -622,9 +668,10 @@ def test_coo_run_sums_on_and_off(A, dtype, runs, monkeypatch):
 
 
 @pytest.mark.parametrize("pattern", ["random", "hub", "banded"])
-@pytest.mark.parametrize("runs", ["0", "1"])
-def test_coo_run_sums_exact_integer_bitwise(pattern, runs, monkeypatch):
-    monkeypatch.setenv("CBSPMV_COO_RUNS", runs)
+@pytest.mark.parametrize("runopt", _RUNOPTS, ids=_runid)
+def test_coo_slices_exact_integer_bitwise(pattern, runopt, monkeypatch):
+    for k, v in runopt.items():
+        monkeypatch.setenv(k, v)
     A = synth.random_csr(300, 260, 0.08, 17, val_mode=2, pattern=pattern)
     x = synth.vector(A.n, synth.VEC_INT7)
     y_ref, _ = oracle.spmv_csr(A, x)
@@ -633,9 +680,16 @@ def test_coo_run_sums_exact_integer_bitwise(pattern, runs, monkeypatch):
         assert np.array_equal(y, y_ref)
 
 
+def test_build_rejects_bad_run_max(monkeypatch):
+    _ok()
+    monkeypatch.setenv("CBSPMV_RUN_MAX", "256")
+    with pytest.raises(cb.CBSpMVError):
+        cb.build(synth.fig1(), device=0)
+
+
 def test_coo_run_sums_on_for_rmat_hubs():
-    """R-MAT's hub rows give many chunks same-row runs (flagged, summed in the warp): the 4096
-    lowest rows (the hubs) and a random sample against the oracle."""
+    """R-MAT's hub rows: long row runs per page, cut into pieces of Lmax and summed in the lanes:
+    the 4096 lowest rows (the hubs) and a random sample against the oracle."""
     _ok()
     A = synth.make("rmat")
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=9)
