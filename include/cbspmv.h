@@ -109,6 +109,8 @@ typedef struct {
   double build_seconds;           /* host pipeline wall time (a1..a7 + device layout) */
   double upload_seconds;          /* H2D copy wall time */
   int32_t n_panels;               /* column panels (1 = whole matrix); counts above sum over panels */
+  int64_t n_hot;                  /* hot x columns cached in shared memory, summed
+                                     over panels; 0 = no cache */
 } cbspmv_info_t;
 
 /* Host copies of the canonical format, slot order (after Alg. 2).  Pointers
@@ -226,6 +228,15 @@ cbspmv_status_t cbspmv_export_panel(cbspmv_handle_t h, int32_t k, cbspmv_export_
  * verification; synchronous; single-panel handles only). */
 cbspmv_status_t cbspmv_download_stream(cbspmv_handle_t h, void *stream_host, size_t stream_bytes,
                                        uint64_t *page_off_host, size_t n_page_off);
+
+/* The hot x columns of panel k (the most frequent COO columns, ascending; a
+ * COO element with column hot[s] stores 0x80000000 | s in the device page stream and reads its
+ * x from a shared-memory copy made at the start of each launch).  *n_hot gets their count;
+ * cols_host (>= *n_hot entries) gets them, unless cols_host is NULL with n_cols 0 (a count
+ * query) or *n_hot is 0.  Layout verification only;
+ * synchronous.  EDIM if cols_host is too small, EINVAL for a bad panel. */
+cbspmv_status_t cbspmv_hot_columns(cbspmv_handle_t h, int32_t k, uint32_t *cols_host, size_t n_cols,
+                                   int64_t *n_hot);
 
 /* ------------------------------------------------------------------ files
  * Host CSR returned by cbspmv_mm_read; its arrays are owned by the library and released

@@ -55,7 +55,7 @@ class Info(ctypes.Structure):
         ("meta_bytes", ctypes.c_int64), ("alg_bytes", ctypes.c_int64), ("dev_stream_bytes", ctypes.c_int64),
         ("n_pages", ctypes.c_int64), ("dev_bytes", ctypes.c_int64), ("grid", ctypes.c_int32),
         ("launches_per_spmv", ctypes.c_int32), ("build_seconds", ctypes.c_double),
-        ("upload_seconds", ctypes.c_double), ("n_panels", ctypes.c_int32),
+        ("upload_seconds", ctypes.c_double), ("n_panels", ctypes.c_int32), ("n_hot", ctypes.c_int64),
     ]
 
 
@@ -114,6 +114,7 @@ def lib():
             "cbspmv_export": ([H, ctypes.POINTER(Export)], i32),
             "cbspmv_export_panel": ([H, i32, ctypes.POINTER(Export)], i32),
             "cbspmv_download_stream": ([H, vp, ctypes.c_size_t, vp, ctypes.c_size_t], i32),
+            "cbspmv_hot_columns": ([H, i32, vp, ctypes.c_size_t, vp], i32),
             "cbspmv_destroy": ([H], i32),
             "cbspmv_mm_read": ([ctypes.c_char_p, ctypes.POINTER(CsrC)], i32),
             "cbspmv_mm_write": ([ctypes.c_char_p, i64, i64, vp, vp, vp], i32),
@@ -377,6 +378,16 @@ def download_stream(h: Handle) -> tuple[np.ndarray, np.ndarray]:
     _check(lib().cbspmv_download_stream(h.raw, s.ctypes.data, s.size, po.ctypes.data, po.size),
            "cbspmv_download_stream")
     return s[:nbytes], po
+
+
+def hot_columns(h: Handle, k: int = 0) -> np.ndarray:
+    """The hot x columns of panel k (cbspmv_hot_columns): slot s of the shared x cache holds x[cols[s]]."""
+    n = ctypes.c_int64(0)
+    _check(lib().cbspmv_hot_columns(h.raw, k, None, 0, ctypes.byref(n)), "cbspmv_hot_columns")
+    out = np.zeros(max(n.value, 1), np.uint32)
+    if n.value:
+        _check(lib().cbspmv_hot_columns(h.raw, k, out.ctypes.data, out.size, ctypes.byref(n)), "cbspmv_hot_columns")
+    return out[:n.value]
 
 
 def destroy(h: Handle) -> None:

@@ -58,6 +58,8 @@ struct Part {
   uint64_t *d_page_off = nullptr;
   uint32_t *d_cta_page = nullptr;
   uint32_t *d_page_ctr = nullptr;
+  uint32_t *d_hot = nullptr;  // hot x columns (shared x cache, cb_internal.h)
+  int64_t n_hot = 0;
   int64_t stream_bytes = 0, n_pages = 0;
   std::unique_ptr<cb::DevCanon> dc;  // device builder: records still on the device until the stream fill
 };
@@ -129,7 +131,8 @@ static void free_device(cbspmv_s *h) {
     cudaFree(p.d_page_off);
     cudaFree(p.d_cta_page);
     cudaFree(p.d_page_ctr);
-    p.d_stream = nullptr; p.d_page_off = nullptr; p.d_cta_page = nullptr; p.d_page_ctr = nullptr;
+    cudaFree(p.d_hot);
+    p.d_stream = nullptr; p.d_page_off = nullptr; p.d_cta_page = nullptr; p.d_page_ctr = nullptr; p.d_hot = nullptr;
   }
   cudaFree(h->d_x_tmp);
   cudaFree(h->d_y_tmp);
@@ -162,11 +165,15 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   // Row-run slices (cb_internal.h): a lane sums its piece of a row's run and issues one RED for
   // it.  Env knobs, read per build, for A/B runs: CBSPMV_RUN_MAX (Lmax, default 8),
   // CBSPMV_COO_RUNS=0 (Lmax = 1: one RED per element), CBSPMV_RUN_ORDER=row (pieces by row instead
-  // of by length).
+  // of by length), CBSPMV_HOT_BYTES (shared x cache budget, 0: none), CBSPMV_HOT_MIN_PCT (share
+  // of the COO elements the cache must serve; 0 forces the cache on).
   cb::SliceOpts so;
   if (const char *v = std::getenv("CBSPMV_RUN_MAX")) so.run_max = std::atoi(v);
+  if (const char *v = std::getenv("CBSPMV_HOT_BYTES")) so.hot_bytes = std::max(0, std::atoi(v));
+  if (const char *v = std::getenv("CBSPMV_HOT_MIN_PCT")) so.hot_min_pct = std::max(0, std::atoi(v));
   if (const char *v = std::getenv("CBSPMV_COO_RUNS"); v && std::atoi(v) == 0) so.run_max = 1;
   if (const char *v = std::getenv("CBSPMV_RUN_ORDER"); v && std::string(v) == "row") so.row_order = 1;
+  so.hot_bytes = std::min(so.hot_bytes, shape.hot_cap);  // what the stages leave of the shared memory
   cb::CooCoords coords;
   if (on_device) {  // the records stay on the device: the slice layout needs the COO coordinates
     st = cb::download_coo_coords(c, *P->dc, cs, &coords, err);
@@ -180,6 +187,7 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   static_cast<CbShape &>(D) = shape;
   D.device = o.device; D.dtype = dtype; D.agg = c.agg; D.m = c.m; D.n = c.n;
   D.n_pages = npages;
+  D.n_hot = (int)S.hot_cols.size();
   st = cb_configure(&D, err);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   // persistent CTA g streams pages [cta[g], cta[g+1]): equal byte shares
@@ -198,6 +206,7 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   if (e == cudaSuccess) e = cudaMalloc(&P->d_cta_page, cta.size() * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&P->d_page_ctr, cb::kCtrSlots * 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemsetAsync(P->d_page_ctr, 0, cb::kCtrSlots * 2 * sizeof(uint32_t), cs);
+  if (e == cudaSuccess && !S.hot_cols.empty()) e = cudaMalloc(&P->d_hot, S.hot_cols.size() * sizeof(uint32_t));
   if (e != cudaSuccess) {
     cudaGetLastError();
     cb::free_stream(&S);
@@ -220,6 +229,8 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
                         cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(P->d_cta_page, cta.data(), cta.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && !S.hot_cols.empty())
+    e = cudaMemcpyAsync(P->d_hot, S.hot_cols.data(), S.hot_cols.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   tm.lap("upload: copies + sync");
   cb::free_stream(&S);
@@ -231,6 +242,8 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   *t_up += now() - t1;
   D.d_stream = P->d_stream; D.d_page_off = P->d_page_off; D.d_cta_page = P->d_cta_page;
   D.d_page_ctr = P->d_page_ctr;
+  D.d_hot = P->d_hot;
+  P->n_hot = (int64_t)S.hot_cols.size();
   P->stream_bytes = (int64_t)total;
   P->n_pages = npages;
   return CBSPMV_OK;
@@ -273,8 +286,9 @@ static void fill_info(cbspmv_s *h, int64_t m, int64_t n, double t0, double t_up,
     loads_nat.insert(loads_nat.end(), c.tb_load_nat.begin(), c.tb_load_nat.end());
     I.dev_stream_bytes += p.stream_bytes;
     I.n_pages += p.n_pages;
-    I.dev_bytes += p.stream_bytes + (p.n_pages + 1) * 8 + (int64_t)(p.dev.grid + 1) * 4;
+    I.dev_bytes += p.stream_bytes + (p.n_pages + 1) * 8 + (int64_t)(p.dev.grid + 1) * 4 + 4 * p.n_hot;
     I.launches_per_spmv += p.n_pages > 0 ? 1 : 0;
+    I.n_hot += p.n_hot;
   }
   I.alg_bytes += (int64_t)h->vec_size * (n + m);
   load_stats(loads, &I.tb_load_mean, &I.tb_load_sd, &I.tb_load_max);
@@ -347,9 +361,11 @@ static cbspmv_status_t build_impl(int64_t m, int64_t n, int64_t nnz, const int64
       int l2 = 0;
       cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, o.device);
       const double xb = (double)n * h->vec_size;
-      // x slices of ~1/5 of L2 (uniform 2^25, 268 MB of x: 6 panels 14.57 ms, 8: 13.28, 10: 13.09,
-      // 12: 13.08, 16: 13.15, 24: 13.64 per SpMV on B200)
-      if (l2 > 0 && xb > 0.75 * l2) P = (int)std::ceil(xb / (0.2 * l2));
+      // x slices of ~1/3 of L2.  Each panel's REDs sweep all of y, so more panels re-read and
+      // re-write y once more each, while a wider x slice misses L2 more (uniform 2^25, 268 MB of x,
+      // per SpMV on B200 with row-run slices and the L1 left to the gathers: 1 panel 26.1 ms,
+      // 3: 13.6, 4: 10.4, 5: 8.68, 6: 8.39, 8: 8.76, 11: 9.2, 16: 9.87, 22: 10.6)
+      if (l2 > 0 && xb > 0.75 * l2) P = (int)std::ceil(xb / (0.36 * l2));
     }
   }
   const int64_t nbc = (n + o.blk - 1) / o.blk;
@@ -693,6 +709,21 @@ cbspmv_status_t cbspmv_download_stream(cbspmv_handle_t h, void *stream_host, siz
   if (p.stream_bytes) e = cudaMemcpy(stream_host, p.d_stream, (size_t)p.stream_bytes, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess)
     e = cudaMemcpy(page_off_host, p.d_page_off, ((size_t)p.n_pages + 1) * 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ECUDA, cudaGetErrorString(e)); }
+  return CBSPMV_OK;
+}
+
+cbspmv_status_t cbspmv_hot_columns(cbspmv_handle_t h, int32_t k, uint32_t *cols_host, size_t n_cols,
+                                   int64_t *n_hot) {
+  if (!h || !n_hot) return fail(CBSPMV_EINVAL, "null argument");
+  if (h->device < 0) return fail(CBSPMV_EUNSUPPORTED, "host-only handle");
+  if (k < 0 || k >= (int32_t)h->parts.size()) return fail(CBSPMV_EINVAL, "panel out of range");
+  const Part &p = h->parts[(size_t)k];
+  *n_hot = p.n_hot;
+  if (p.n_hot == 0 || (!cols_host && n_cols == 0)) return CBSPMV_OK;  // count query
+  if (!cols_host || n_cols < (size_t)p.n_hot) return fail(CBSPMV_EDIM, "destination too small");
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaMemcpy(cols_host, p.d_hot, (size_t)p.n_hot * 4, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) { cudaGetLastError(); return fail(CBSPMV_ECUDA, cudaGetErrorString(e)); }
   return CBSPMV_OK;
 }

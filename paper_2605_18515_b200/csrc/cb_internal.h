@@ -55,6 +55,10 @@ struct NvtxRange {
 //                in the stage (non-aggregated only: 16 values after the page, filled by TMA)
 //   COO slice:   a = table offset | nl << 16 | w << 24 (w = longest piece); b = cols offset |
 //                vals offset << 16; c = E (elements); d = 0
+// Hot x columns: when a few columns carry a large share of the COO elements (power-law graphs),
+// the builder lists the H most frequent ones (Stream::hot_cols, ascending) and a slice element
+// whose column is hot stores kHotBit | slot instead of the column; each CTA copies x[hot_cols[]]
+// into shared memory at the start of a launch and reads those elements' x from there.
 // ---------------------------------------------------------------------------
 #ifdef __CUDACC__
 #define CB_HD __host__ __device__
@@ -69,6 +73,9 @@ constexpr int kDefaultRunMax = 8;          // Lmax (env CBSPMV_RUN_MAX, read per
 constexpr uint32_t kEndItems = 0xFFFFFFFFu;  // header.nitems of the dynamic-claiming end marker
 constexpr int kMaxPageCap = 65536;         // descriptor offsets are u16 bytes
 constexpr int kCtrSlots = 64;              // page-claim counters per panel (launch k uses slot k % 64)
+constexpr uint32_t kHotBit = 0x80000000u;  // slice column = kHotBit | slot of a hot x column
+constexpr int kDefaultHotBytes = 65536;    // shared x cache (env CBSPMV_HOT_BYTES, read per build)
+constexpr int kDefaultHotMinPct = 5;       // cache only if it serves >= this share of the COO elements
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 // bytes of a slice table (rows u32[nl] | lens u8[nl], 4-aligned) and of its elements (cols u32[E]
@@ -128,6 +135,7 @@ struct Stream {
   bool pinned = false;
   int64_t nbytes = 0;
   std::vector<uint64_t> page_off;  // n_pages + 1
+  std::vector<uint32_t> hot_cols;  // hot x columns (ascending; slot = index), empty: no x cache
 };
 // Device-fill plan of the page stream (device builder): the page prefixes (header | item
 // descriptors | slice tables) in a compact buffer, per slot-order block the stream offset of its
@@ -153,6 +161,8 @@ struct CooCoords {
 struct SliceOpts {
   int run_max = kDefaultRunMax;  // 1: every element its own piece (no in-lane run sums; A/B)
   int row_order = 0;             // 0: pieces by (length desc, row asc); 1: by row asc
+  int hot_bytes = kDefaultHotBytes;   // shared x cache budget (0: none)
+  int hot_min_pct = kDefaultHotMinPct;
 };
 // x_size: bytes of one x element (sizes the x area that follows each page in its stage).
 // plan == nullptr: the whole stream is written to host memory (s->bytes); otherwise only the plan.
@@ -170,6 +180,7 @@ struct DevCanon {
 };
 // Write the device page stream (d_stream, s.nbytes) from the plan and the device-resident records
 // (gpu_builder.cu): page prefixes, restore entries, records (DENSE in the lane-major layout).
+// (hot x columns: the slice columns are encoded from s.hot_cols on the device as well)
 int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, const StreamPlan &plan, void *stream,
                        uint8_t *d_stream, std::string *err);
 // The coordinate bytes of the slot-order COO blocks from the device-resident records.
@@ -227,10 +238,13 @@ int resolve_threads(int t);
 // G consumer groups (G divides S) of W warps, X x warps (X <= G).
 struct CbShape {
   int nstage = 12, groups = 4, gwarps = 7, xwarps = 3, page_cap = 19008;
+  int hot_cap = 0;  // shared memory left for the hot x cache (bytes)
 };
 
 struct CbDevice : CbShape {
   int device = -1;
+  int n_hot = 0;                          // hot x columns (shared x cache), 0: none
+  const uint32_t *d_hot = nullptr;        // their indices (device)
   int dtype = 0;
   int agg = 0;
   int64_t m = 0, n = 0;

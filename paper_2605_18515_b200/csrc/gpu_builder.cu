@@ -531,7 +531,7 @@ __global__ void k_coo(int64_t nb, const int32_t *__restrict__ br, const int32_t 
                       const int64_t *__restrict__ e0, const uint32_t *__restrict__ dst,
                       const uint64_t *__restrict__ page, const uint8_t *__restrict__ mtx,
                       const uint32_t *__restrict__ restore, const uint64_t *__restrict__ coff, int agg,
-                      uint8_t *__restrict__ stream) {
+                      const uint32_t *__restrict__ hot, uint8_t *__restrict__ stream) {
   constexpr int S = (int)sizeof(W);
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -546,10 +546,18 @@ __global__ void k_coo(int64_t nb, const int32_t *__restrict__ br, const int32_t 
     for (int e = lane; e < k; e += 32) {
       const uint32_t d = dst[e0[b] + e];
       const uint32_t cb = coord[e];  // (col << 4) | row
-      *reinterpret_cast<uint32_t *>(pg + (d & 0xFFFFu)) = seg ? seg[cb >> 4] : (uint32_t)bc[b] * kBlk + (cb >> 4);
+      uint32_t col = seg ? seg[cb >> 4] : (uint32_t)bc[b] * kBlk + (cb >> 4);
+      if (hot && hot[col] != 0xFFFFFFFFu) col = kHotBit | hot[col];  // cached x column (cb_internal.h)
+      *reinterpret_cast<uint32_t *>(pg + (d & 0xFFFFu)) = col;
       *reinterpret_cast<W *>(pg + (d >> 16)) = vals[e];
     }
   }
+}
+
+// column -> slot of the hot x columns (the rest of the map is 0xFF-filled)
+__global__ void k_hot_map(const uint32_t *__restrict__ cols, int64_t n_hot, uint32_t *__restrict__ map) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_hot; k += (int64_t)gridDim.x * blockDim.x)
+    map[cols[k]] = (uint32_t)k;
 }
 
 // one warp per COO block: its coordinate bytes into the compact download buffer
@@ -579,7 +587,7 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
   const int64_t npages = (int64_t)s.page_off.size() - 1, nb = c.nb;
   if (s.nbytes > 0 && !x.ok(cudaMemsetAsync(d_stream, 0, (size_t)s.nbytes, x.st), "memset stream")) return x.status;
   if (npages <= 0) return x.ok(cudaStreamSynchronize(x.st), "sync") ? CBSPMV_OK : x.status;
-  DBuf d_meta, d_moff, d_poff, d_br, d_bc, d_nnz, d_type, d_vp, d_rdst, d_sdst, d_ncol, d_e0, d_dst;
+  DBuf d_meta, d_moff, d_poff, d_br, d_bc, d_nnz, d_type, d_vp, d_rdst, d_sdst, d_ncol, d_e0, d_dst, d_hc, d_hmap;
   if (!upload_vec(x, d_meta, plan.meta, "upload plan") || !upload_vec(x, d_moff, plan.meta_off, "upload plan") ||
       !upload_vec(x, d_poff, s.page_off, "upload plan") || !upload_vec(x, d_br, c.br, "upload plan") ||
       !upload_vec(x, d_bc, c.bc, "upload plan") || !upload_vec(x, d_nnz, c.nnzb, "upload plan") ||
@@ -588,6 +596,13 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
       (c.agg && !upload_vec(x, d_sdst, plan.res_dst, "upload plan")) ||
       !upload_vec(x, d_e0, plan.coo_e0, "upload plan") || !upload_vec(x, d_dst, plan.coo_dst, "upload plan"))
     return x.status;
+  const int64_t n_hot = (int64_t)s.hot_cols.size();
+  if (n_hot > 0) {
+    if (!upload_vec(x, d_hc, s.hot_cols, "upload hot columns") || !x.alloc(d_hmap, 4 * (size_t)c.n, "alloc hot map") ||
+        !x.ok(cudaMemsetAsync(d_hmap.p, 0xFF, 4 * (size_t)c.n, x.st), "memset hot map"))
+      return x.status;
+    k_hot_map<<<grid_for(n_hot, 256), 256, 0, x.st>>>(d_hc.as<uint32_t>(), n_hot, d_hmap.as<uint32_t>());
+  }
   k_prefix<<<(int)std::min<int64_t>(npages, 148 * 16), 128, 0, x.st>>>(d_meta.as<uint8_t>(), d_moff.as<uint64_t>(),
                                                                       d_poff.as<uint64_t>(), npages, d_stream);
   if (nb > 0) {
@@ -599,7 +614,7 @@ int fill_stream_device(const Canon &c, const DevCanon &dc, const Stream &s, cons
                                     d_ncol.as<int32_t>(), dc.mtx, dc.restore, dc.cols_offset, d_stream);               \
   k_coo<W><<<g, 256, 0, x.st>>>(nb, d_br.as<int32_t>(), d_bc.as<int32_t>(), d_nnz.as<int32_t>(), d_vp.as<uint64_t>(), \
                                 d_e0.as<int64_t>(), d_dst.as<uint32_t>(), d_rdst.as<uint64_t>(), dc.mtx, dc.restore,  \
-                                dc.cols_offset, c.agg, d_stream)
+                                dc.cols_offset, c.agg, n_hot ? d_hmap.as<uint32_t>() : nullptr, d_stream)
     if (c.val_size == 8) {
       CB_FILL(uint64_t);
     } else {

@@ -158,10 +158,11 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
 // lanes whose piece is longer than j read their element (index off_j + rank among those lanes),
 // gather x[col] into a register (ld.global.nc, L2 evict_last) and accumulate; then one RED per
 // piece (Alg. 3's atomicAdd).  B slices (items da0, da0 + dstride, ...) advance together so B
-// gathers per lane are in flight.
+// gathers per lane are in flight.  An element whose column carries kHotBit reads its x from the
+// CTA's shared copy of the hot x columns (hotx: its shared address).
 template <typename M, typename V, bool SCALED, int B>
 __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t dstride, const V *__restrict__ x,
-                                           V *__restrict__ y, V scale, int lane, uint64_t pol, Dbg dbg) {
+                                           uint32_t hotx, V *__restrict__ y, V scale, int lane, uint64_t pol, Dbg dbg) {
   uint32_t cv[B], off[B], row[B];  // cv: cols offset | vals offset << 16 (page-relative)
   int len[B];
   V acc[B];
@@ -180,25 +181,32 @@ __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t d
   }
   const unsigned below = (1u << lane) - 1u;
   for (int j = 0; j < wmax; j++) {
-    V xv[B];
-    uint32_t va[B];  // shared address of the lane's value (its load waits until the gathers are issued)
+    // the B slices' element indices first, then their column loads, then the gathers: no shared
+    // load waits between two gathers
+    uint32_t ix[B], c[B];
+    bool on[B];
 #pragma unroll
     for (int b = 0; b < B; b++) {
-      xv[b] = V(0);
-      va[b] = 0;
-      const bool on = len[b] > j;
-      const unsigned act = __ballot_sync(kFull, on);
-      if (on) {
-        const uint32_t ix = off[b] + (uint32_t)__popc(act & below);
-        const uint32_t c = lds_u32(pg + (cv[b] & 0xFFFFu) + 4u * ix);
-        va[b] = pg + (cv[b] >> 16) + (uint32_t)sizeof(M) * ix;
-        xv[b] = (dbg.skip() & 2) ? V(1) + V(c & 1) : ldg_x(x + c, pol);
-      }
+      on[b] = len[b] > j;
+      const unsigned act = __ballot_sync(kFull, on[b]);
+      ix[b] = off[b] + (uint32_t)__popc(act & below);
       off[b] += (uint32_t)__popc(act);
     }
 #pragma unroll
+    for (int b = 0; b < B; b++) c[b] = on[b] ? lds_u32(pg + (cv[b] & 0xFFFFu) + 4u * ix[b]) : 0u;
+    V xv[B];
+#pragma unroll
+    for (int b = 0; b < B; b++) {
+      const bool hot = (c[b] & cb::kHotBit) != 0;
+      V g = V(0), h = V(0);
+      if (dbg.skip() & 2) g = V(1) + V(c[b] & 1);
+      else if (on[b] && !hot) g = ldg_x(x + c[b], pol);
+      if (on[b] && hot) h = lds_val<V>(hotx + (uint32_t)sizeof(V) * (c[b] & ~cb::kHotBit));  // shared x cache
+      xv[b] = hot ? h : g;
+    }
+#pragma unroll
     for (int b = 0; b < B; b++)
-      if (va[b]) acc[b] = fma(V(lds_val<M>(va[b])), xv[b], acc[b]);
+      if (on[b]) acc[b] = fma(V(lds_val<M>(pg + (cv[b] >> 16) + (uint32_t)sizeof(M) * ix[b])), xv[b], acc[b]);
   }
 #pragma unroll
   for (int b = 0; b < B; b++) {
@@ -306,6 +314,8 @@ struct KParams {
   int agg;     // aggregated: x gathered by the consumers (restore entries / chunk columns)
   int xvec;    // non-aggregated tiles: x 16-byte aligned -> TMA bulk tile copies
   int xwarps;  // X x warps (X <= G; 0 for aggregated matrices)
+  const uint32_t *hot;  // hot x columns (shared x cache), n_hot of them
+  int n_hot;
   Dbg dbg;
 };
 
@@ -486,6 +496,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   const int cw = warp - 1 - P.xwarps;
   V *wscratch = reinterpret_cast<V *>(smem + kSmemHeader + (size_t)S * P.stage) + cw * 16;
   const uint64_t xpol = policy_evict_last();
+  // the shared x cache: x[hot[s]] for the launch's hot columns, copied by the consumers before
+  // their first page (named barrier 1 over the consumer warps; the producer is already streaming)
+  V *hotx = reinterpret_cast<V *>(smem + kSmemHeader + (size_t)S * P.stage + (size_t)G * W * 16 * 8);
+  if (P.n_hot > 0) {
+    const int nct = 32 * G * W;
+    for (int i = cw * 32 + lane; i < P.n_hot; i += nct) hotx[i] = ldg_x(x + P.hot[i], xpol);
+    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
+  }
+  const uint32_t hota = smem_addr(hotx);
   const int grp = cw / W, wg = cw - grp * W;
   int s = grp;
   uint32_t parity = 0;
@@ -510,13 +529,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     }
     // COO slices, four at a time: the four slices' element loads and x gathers in flight together
     const uint32_t pg = smem_addr(page), dsc = pg + cb::kPageHeader, dW = 16u * (uint32_t)W;
-    for (; k + 3 * W < n; k += 4 * W) coo_slices<M, V, SCALED, 4>(pg, dsc + 16u * (uint32_t)k, dW, x, y, scale, lane, xpol, dbg);
+    for (; k + 3 * W < n; k += 4 * W)
+      coo_slices<M, V, SCALED, 4>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg);
     if (k + W < n) {
-      coo_slices<M, V, SCALED, 2>(pg, dsc + 16u * (uint32_t)k, dW, x, y, scale, lane, xpol, dbg);
+      coo_slices<M, V, SCALED, 2>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg);
       k += 2 * W;
     }
     if (k < n) {
-      coo_slices<M, V, SCALED, 1>(pg, dsc + 16u * (uint32_t)k, dW, x, y, scale, lane, xpol, dbg);
+      coo_slices<M, V, SCALED, 1>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg);
       k += W;
     }
     if (n != (int)nitems) k += ((int)nitems - k + W - 1) / W * W;  // ablation skipped the items
@@ -572,6 +592,10 @@ inline int cuda_fail(cudaError_t e, const char *what, std::string *err) {
 
 // per consumer warp: one 16-value x tile (aggregated CSR / DENSE blocks), fp64-sized
 inline int scratch_bytes(const CbShape &sh) { return sh.groups * sh.gwarps * 16 * 8; }
+// dynamic shared memory of a launch: mbarriers | S stages | warp scratch | hot x cache
+inline int smem_bytes(const CbDevice &d) {
+  return kSmemHeader + d.nstage * d.page_cap + scratch_bytes(d) + d.n_hot * vec_bytes(d.dtype);
+}
 
 int env_int(const char *k, int d) {
   const char *v = std::getenv(k);
@@ -621,6 +645,7 @@ int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err) {
   sh->gwarps = W;
   sh->xwarps = X;
   sh->page_cap = cap;
+  sh->hot_cap = std::max(0, optin - kSmemHeader - S * cap - scratch_bytes(probe));
   return CBSPMV_OK;
 }
 
@@ -628,9 +653,9 @@ int cb_configure(CbDevice *dev, std::string *err) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute", err);
-  const int smem = kSmemHeader + dev->nstage * dev->page_cap + scratch_bytes(*dev);
+  const int smem = smem_bytes(*dev);
   if (smem > optin) {
-    *err = "stages do not fit the shared memory";
+    *err = "stages and the hot x cache do not fit the shared memory";
     return CBSPMV_EUNSUPPORTED;
   }
   for (int dt = 0; dt < 3; dt++)
@@ -683,9 +708,9 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     }
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.claim_chunk,
               ctr ? 0 : dev.strided, dev.m, sumsq, dev.page_cap, dev.nstage, dev.groups, dev.gwarps, dev.agg,
-              !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps,
+              !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps, dev.d_hot, dev.n_hot,
               Dbg{dev.dbg_skip}};
-    const int smem = kSmemHeader + dev.nstage * dev.page_cap + scratch_bytes(dev);
+    const int smem = smem_bytes(dev);
     const void *fn = select_kernel(dev.dtype, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
     const int threads = 32 * (1 + dev.xwarps + dev.groups * dev.gwarps);

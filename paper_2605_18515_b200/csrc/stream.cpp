@@ -10,6 +10,8 @@
 // block leaves >= 50 % of its lanes idle, and issues one atomic per element).
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <memory>
 #include <cstring>
 #include <vector>
 
@@ -151,6 +153,71 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     }
   });
   tm.lap("stream: block row counts");
+  // ---- hot x columns (shared x cache, cb_internal.h): the H columns carrying the most COO
+  // elements, when they carry at least hot_min_pct % of them and save more gathers than the
+  // per-launch cache fill costs (H loads per CTA)
+  auto resolved = [&](int64_t i, uint8_t b) -> uint32_t {
+    return c.agg ? c.restore[c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk + (b >> 4)]
+                 : (uint32_t)c.bc[i] * (uint32_t)c.blk + (b >> 4);
+  };
+  std::vector<uint32_t> hot_slot;  // column -> slot (kNotHot: not cached); empty: no cache
+  constexpr uint32_t kNotHot = 0xFFFFFFFFu;
+  s->hot_cols.clear();
+  {
+    const int64_t H = so.hot_bytes > 0 ? so.hot_bytes / x_size : 0;
+    int64_t n_coo = 0;
+    for (int64_t i = 0; i < c.nb; i++) n_coo += c.type[i] == CBSPMV_FMT_COO ? c.nnzb[i] : 0;
+    const bool force = so.hot_min_pct == 0;
+    if (H > 0 && n_coo > 0 && c.n <= (int64_t)1 << 28 && (force || n_coo >= 4 * 148 * H)) {
+      // estimate on every 64th COO block first (uniform-like matrices stop here)
+      std::vector<uint32_t> samp;
+      for (int64_t i = 0; i < c.nb; i += 64)
+        if (c.type[i] == CBSPMV_FMT_COO)
+          for (int e = 0; e < c.nnzb[i]; e++) samp.push_back(resolved(i, coord(i)[e]));
+      std::sort(samp.begin(), samp.end());
+      std::vector<int64_t> sc;
+      for (size_t a = 0, b; a < samp.size(); a = b) {
+        for (b = a; b < samp.size() && samp[b] == samp[a]; b++) {}
+        sc.push_back((int64_t)(b - a));
+      }
+      const size_t top = std::min(sc.size(), (size_t)H);
+      std::partial_sort(sc.begin(), sc.begin() + top, sc.end(), std::greater<int64_t>());
+      int64_t est = 0;
+      for (size_t k = 0; k < top; k++) est += sc[k];
+      if (force || (int64_t)samp.size() == 0 || est * 100 >= (int64_t)so.hot_min_pct * (int64_t)samp.size()) {
+        // exact column counts of the COO elements
+        std::unique_ptr<std::atomic<uint32_t>[]> hist(new std::atomic<uint32_t>[(size_t)c.n]);
+        parallel_for(c.n, T, 1 << 16, [&](int64_t lo, int64_t hi, int) {
+          for (int64_t j = lo; j < hi; j++) hist[j].store(0, std::memory_order_relaxed);
+        });
+        parallel_for(c.nb, T, 1 << 12, [&](int64_t lo, int64_t hi, int) {
+          for (int64_t i = lo; i < hi; i++)
+            if (c.type[i] == CBSPMV_FMT_COO)
+              for (int e = 0; e < c.nnzb[i]; e++) hist[resolved(i, coord(i)[e])].fetch_add(1, std::memory_order_relaxed);
+        });
+        std::vector<uint32_t> cand;
+        for (int64_t j = 0; j < c.n; j++)
+          if (hist[j].load(std::memory_order_relaxed)) cand.push_back((uint32_t)j);
+        auto more = [&](uint32_t a, uint32_t b) {  // count desc, column asc
+          const uint32_t ca = hist[a].load(std::memory_order_relaxed), cb = hist[b].load(std::memory_order_relaxed);
+          return ca != cb ? ca > cb : a < b;
+        };
+        if ((int64_t)cand.size() > H) {
+          std::nth_element(cand.begin(), cand.begin() + H, cand.end(), more);
+          cand.resize((size_t)H);
+        }
+        int64_t covered = 0;
+        for (uint32_t j : cand) covered += hist[j].load(std::memory_order_relaxed);
+        if (force || (covered * 100 >= (int64_t)so.hot_min_pct * n_coo && covered >= 4 * 148 * (int64_t)cand.size())) {
+          std::sort(cand.begin(), cand.end());
+          hot_slot.assign((size_t)c.n, kNotHot);
+          for (size_t k = 0; k < cand.size(); k++) hot_slot[cand[k]] = (uint32_t)k;
+          s->hot_cols = std::move(cand);
+        }
+      }
+    }
+  }
+  tm.lap("stream: hot x columns");
   // ---- greedy page cut: consecutive slot-order blocks while page + x area fits the stage
   std::vector<int64_t> pb{0};  // first block of each page (+ nb)
   {
@@ -402,9 +469,8 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
               continue;
             }
             const int64_t k = c.nnzb[i];
-            const uint8_t b = coord(i)[E.e];  // (col << 4) | row
-            const uint32_t col = c.agg ? c.restore[c.cols_offset[c.br[i]] + (uint64_t)c.bc[i] * c.blk + (b >> 4)]
-                                       : (uint32_t)c.bc[i] * (uint32_t)c.blk + (b >> 4);
+            uint32_t col = resolved(i, coord(i)[E.e]);  // coordinate byte (col << 4) | row
+            if (!hot_slot.empty() && hot_slot[col] != kNotHot) col = kHotBit | hot_slot[col];
             std::memcpy(page + co, &col, 4);
             std::memcpy(page + vo, c.mtx.data() + c.vp[i] + round_up(k, S) + (int64_t)S * E.e, (size_t)S);
           }

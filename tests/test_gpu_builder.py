@@ -171,11 +171,16 @@ def test_exact_integer_bitwise_device_built(pattern):
 
 @pytest.mark.parametrize("A", CORPUS[::3], ids=lambda A: A.name)
 @pytest.mark.parametrize("run_max", ["1", "3", "32"])
-def test_device_built_coo_slices(A, run_max, monkeypatch):
+@pytest.mark.parametrize("hot", ["", "256"])
+def test_device_built_coo_slices(A, run_max, hot, monkeypatch):
     """Row-run slices filled on the device (k_coo at the host plan's offsets) on device-built
-    handles, for several Lmax; the stream-decode test checks the layout itself."""
+    handles, for several Lmax, with and without a forced 32-column hot x cache; the stream-decode
+    test checks the layout itself."""
     _ok()
     monkeypatch.setenv("CBSPMV_RUN_MAX", run_max)
+    if hot:
+        monkeypatch.setenv("CBSPMV_HOT_MIN_PCT", "0")
+        monkeypatch.setenv("CBSPMV_HOT_BYTES", hot)
     x = synth.vector(A.n, synth.VEC_UNIFORM, seed=12)
     y_ref, R = oracle.spmv_csr(A, x)
     for agg in (0, 1):

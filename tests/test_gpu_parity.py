@@ -224,14 +224,18 @@ def decode_stream(stream, page_off):
     return pages
 
 
-def decode_slice(pg, it, S, vdt):
+def decode_slice(pg, it, S, vdt, hot=None):
     """One COO slice: its pieces (row, length) and, per piece, its elements (column, value) in step
-    order -- element (lane l, step j) at off_j + (lanes below l whose piece is longer than j)."""
+    order -- element (lane l, step j) at off_j + (lanes below l whose piece is longer than j); a
+    column with bit 31 set is slot s of the hot x columns (cb.hot_columns)."""
     nl = it["nl"]
     rows = pg[it["tab"]:it["tab"] + 4 * nl].view(np.uint32).astype(np.int64)
     lens = pg[it["tab"] + 4 * nl:it["tab"] + 5 * nl].astype(np.int64)
     E = int(lens.sum())
     cols = pg[it["cols"]:it["cols"] + 4 * E].view(np.uint32).astype(np.int64)
+    is_hot = cols >= 1 << 31
+    if is_hot.any():
+        cols[is_hot] = hot[cols[is_hot] - (1 << 31)]
     vals = pg[it["vals"]:it["vals"] + S * E].view(vdt)
     elems = [[] for _ in range(nl)]
     off = 0
@@ -261,7 +265,8 @@ def _long_run_matrix():
                                   "corpus_diag"])
 @pytest.mark.parametrize("dtype", ["f64", "f32f64"])
 @pytest.mark.parametrize("device_build", [0, 1])
-@pytest.mark.parametrize("runopt", ["", "RUN_MAX=7", "RUN_MAX=32", "RUN_ORDER=row"])
+@pytest.mark.parametrize("runopt", ["", "RUN_MAX=7", "RUN_MAX=32", "RUN_ORDER=row", "HOT_MIN_PCT=0",
+                                    "HOT_MIN_PCT=0,HOT_BYTES=256"])
 def test_device_stream_encodes_canonical_format(name, dtype, device_build, runopt, monkeypatch):
     """What is on the device is exactly the canonical format (slot order): pages tile the slot
     order; CSR / DENSE records byte-equal (DENSE re-laid lane-major), their restore entries equal
@@ -271,8 +276,8 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build, runop
     per slice.  device_build=1: the stream is filled on the device from the device-built records."""
     _ok()
     run_max = 8  # kDefaultRunMax
-    if runopt:
-        k, v = runopt.split("=")
+    for kv in filter(None, runopt.split(",")):
+        k, v = kv.split("=")
         monkeypatch.setenv("CBSPMV_" + k, v)
         run_max = int(v) if k == "RUN_MAX" else run_max
     row_order = runopt == "RUN_ORDER=row"
@@ -290,6 +295,12 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build, runop
     h = cb.build(A, dtype=dtype, device=0, device_build=device_build, **opts)
     ex = cb.export(h)
     s, po = cb.download_stream(h)
+    hot = cb.hot_columns(h).astype(np.int64)
+    assert h.info["n_hot"] == len(hot) and np.all(np.diff(hot) > 0)
+    if runopt.startswith("HOT_MIN_PCT=0") and h.info["agg"]:  # forced cache (non-aggregated: no room)
+        n_coo = int(np.sum(ex["nnz_per_blk"][ex["type_per_blk"] == 0]))
+        assert (len(hot) > 0) == (n_coo > 0)
+        assert len(hot) <= (32 if "HOT_BYTES" in runopt else 8192)
     if name == "one_block_row":
         assert ex["nb"] == 40
     pages = decode_stream(s, po)
@@ -358,7 +369,7 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build, runop
         tab = 16 + 16 * P["nitems"]
         for n_s, it in enumerate(slices):
             assert it["d"] == 0 and it["tab"] == tab
-            rows, lens, elems = decode_slice(pg, it, S, vdt)
+            rows, lens, elems = decode_slice(pg, it, S, vdt, hot)
             tab += (5 * it["nl"] + 3) // 4 * 4
             assert 1 <= it["nl"] <= 32 and (it["nl"] == 32 or n_s == len(slices) - 1)
             assert np.all(lens >= 1) and np.all(lens <= run_max)
@@ -643,7 +654,9 @@ def test_spmv_host_batch_pipelined(count, dtype):
 
 
 _RUNOPTS = [{"CBSPMV_COO_RUNS": "0"}, {"CBSPMV_RUN_MAX": "1"}, {"CBSPMV_RUN_MAX": "2"}, {"CBSPMV_RUN_MAX": "5"},
-            {}, {"CBSPMV_RUN_MAX": "32"}, {"CBSPMV_RUN_MAX": "255"}, {"CBSPMV_RUN_ORDER": "row"}, {"CBSPMV_RUN_ORDER": "row", "CBSPMV_RUN_MAX": "3"}]
+            {}, {"CBSPMV_RUN_MAX": "32"}, {"CBSPMV_RUN_MAX": "255"}, {"CBSPMV_RUN_ORDER": "row"},
+            {"CBSPMV_RUN_ORDER": "row", "CBSPMV_RUN_MAX": "3"}, {"CBSPMV_HOT_MIN_PCT": "0"},
+            {"CBSPMV_HOT_MIN_PCT": "0", "CBSPMV_HOT_BYTES": "256"}, {"CBSPMV_HOT_BYTES": "0"}]
 _runid = lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()) or "default"
 
 
