@@ -70,10 +70,10 @@ inline int val_bytes(int dtype) { return dtype == CBSPMV_F64 ? 8 : 4; }
 inline int vec_bytes(int dtype) { return dtype == CBSPMV_F32 ? 4 : 8; }
 inline bool valid_dtype(int dtype) { return dtype == CBSPMV_F64 || dtype == CBSPMV_F32 || dtype == CBSPMV_F32F64; }
 
-struct SubCsr {
-  std::vector<int64_t> rp;
-  std::vector<int32_t> col;
-  std::vector<uint8_t> val;  // raw bytes of the value type
+struct SubCsr {  // no value-initialisation: the parallel copies write every element
+  std::vector<int64_t, cb::NoInitAlloc<int64_t>> rp;
+  std::vector<int32_t, cb::NoInitAlloc<int32_t>> col;
+  cb::ByteBuf val;  // raw bytes of the value type
 };
 
 }  // namespace
@@ -384,9 +384,10 @@ static cbspmv_status_t build_impl(int64_t m, int64_t n, int64_t nnz, const int64
     st = cb::check_csr(A, o, &nz, &err);  // the split below relies on sorted, in-range columns
     for (int k = 0; k < P && st == CBSPMV_OK; k++) {
       SubCsr sub;
-      sub.rp.assign((size_t)m + 1, 0);
+      sub.rp.resize((size_t)m + 1);
+      sub.rp[0] = 0;
       const int64_t c0 = cuts[k], c1 = cuts[k + 1];
-      std::vector<int64_t> lo(m), hi(m);
+      std::vector<int64_t, cb::NoInitAlloc<int64_t>> lo((size_t)m), hi((size_t)m);
       cb::parallel_for(m, o.host_threads, 1 << 14, [&](int64_t a, int64_t b, int) {
         for (int64_t i = a; i < b; i++) {
           const int32_t *rb = col_idx + row_ptr[i], *re = col_idx + row_ptr[i + 1];

@@ -169,9 +169,9 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     for (int64_t i = 0; i < c.nb; i++) n_coo += c.type[i] == CBSPMV_FMT_COO ? c.nnzb[i] : 0;
     const bool force = so.hot_min_pct == 0;
     if (H > 0 && n_coo > 0 && c.n <= (int64_t)1 << 28 && (force || n_coo >= 4 * 148 * H)) {
-      // estimate on every 64th COO block first (uniform-like matrices stop here)
+      // estimate on every 251st COO block first (uniform-like matrices stop here)
       std::vector<uint32_t> samp;
-      for (int64_t i = 0; i < c.nb; i += 64)
+      for (int64_t i = 0; i < c.nb; i += 251)
         if (c.type[i] == CBSPMV_FMT_COO)
           for (int e = 0; e < c.nnzb[i]; e++) samp.push_back(resolved(i, coord(i)[e]));
       std::sort(samp.begin(), samp.end());
@@ -218,41 +218,60 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     }
   }
   tm.lap("stream: hot x columns");
-  // ---- greedy page cut: consecutive slot-order blocks while page + x area fits the stage
-  std::vector<int64_t> pb{0};  // first block of each page (+ nb)
-  {
-    PageAcc cur;
+  // ---- greedy page cut: consecutive slot-order blocks while page + x area fits the stage.  Large
+  // matrices are cut in fixed segments of >= 2^16 blocks, in parallel (a page does not cross a
+  // segment start; the segments do not depend on the thread count, so the stream does not either).
+  const int64_t seg_len = std::max<int64_t>(1 << 16, ceil_div(c.nb, 64));
+  const int64_t nseg = std::max<int64_t>(1, ceil_div(c.nb, seg_len));
+  std::vector<std::vector<int64_t>> seg_pb((size_t)nseg);
+  std::vector<int> seg_fail((size_t)nseg, 0);
+  parallel_for(nseg, T, 1, [&](int64_t lo, int64_t hi, int) {
     BrTable tab;
-    for (int64_t i = 0; i < c.nb; i++) {
-      PageAcc nx = cur;
-      int slot = -1;
-      if (c.type[i] == CBSPMV_FMT_COO) {
-        slot = tab.find(c.br[i]);
-        for (int r = 0; r < 16; r++) {
-          const int64_t o = slot >= 0 ? tab.counts(slot)[r] : 0, k = rcnt[i][r];
-          nx.P += sh.pieces(o + k) - sh.pieces(o);
-        }
-        nx.E += c.nnzb[i];
-      } else {
-        nx.items++; nx.rec += rec[i]; nx.xb += c.agg ? 0 : 16 * (int64_t)x_size;
-      }
-      nx.blocks++;
-      if (sh.stage_bytes(nx) <= page_cap) {
-        cur = nx;
-        if (c.type[i] == CBSPMV_FMT_COO) {
-          if (slot < 0) slot = tab.insert(c.br[i]);
-          for (int r = 0; r < 16; r++) tab.counts(slot)[r] += rcnt[i][r];
-        }
-        continue;
-      }
-      if (cur.blocks == 0) { *err = "stage capacity too small for one block"; return CBSPMV_EUNSUPPORTED; }
-      pb.push_back(i);
-      cur = PageAcc{};
+    for (int64_t sg = lo; sg < hi; sg++) {
+      const int64_t b0 = sg * seg_len, b1 = std::min(c.nb, b0 + seg_len);
+      std::vector<int64_t> &out = seg_pb[(size_t)sg];
+      PageAcc cur;
       tab.clear();
-      i--;  // re-add block i to the empty page
+      for (int64_t i = b0; i < b1; i++) {
+        PageAcc nx = cur;
+        int slot = -1;
+        if (c.type[i] == CBSPMV_FMT_COO) {
+          slot = tab.find(c.br[i]);
+          for (int r = 0; r < 16; r++) {
+            const int64_t o = slot >= 0 ? tab.counts(slot)[r] : 0, k = rcnt[i][r];
+            nx.P += sh.pieces(o + k) - sh.pieces(o);
+          }
+          nx.E += c.nnzb[i];
+        } else {
+          nx.items++; nx.rec += rec[i]; nx.xb += c.agg ? 0 : 16 * (int64_t)x_size;
+        }
+        nx.blocks++;
+        if (sh.stage_bytes(nx) <= page_cap) {
+          cur = nx;
+          if (c.type[i] == CBSPMV_FMT_COO) {
+            if (slot < 0) slot = tab.insert(c.br[i]);
+            for (int r = 0; r < 16; r++) tab.counts(slot)[r] += rcnt[i][r];
+          }
+          continue;
+        }
+        if (cur.blocks == 0) { seg_fail[(size_t)sg] = 1; break; }
+        out.push_back(i);  // block i starts a new page
+        cur = PageAcc{};
+        tab.clear();
+        i--;  // re-add block i to the empty page
+      }
     }
-    if (c.nb > pb.back()) pb.push_back(c.nb);
+  });
+  for (int f : seg_fail)
+    if (f) { *err = "stage capacity too small for one block"; return CBSPMV_EUNSUPPORTED; }
+  std::vector<int64_t> pb;  // first block of each page (+ nb)
+  for (int64_t sg = 0; sg < nseg; sg++) {
+    if (sg * seg_len < c.nb) pb.push_back(sg * seg_len);
+    pb.insert(pb.end(), seg_pb[(size_t)sg].begin(), seg_pb[(size_t)sg].end());
   }
+  if (pb.empty()) pb.push_back(0);
+  pb.push_back(c.nb);
+  if (c.nb == 0) pb.assign(1, 0);
   const int64_t npages = (int64_t)pb.size() - 1;
   tm.lap("stream: page cut");
 
@@ -351,21 +370,31 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     std::vector<int64_t> cd;                 // CSR / DENSE blocks of the page
     std::vector<Elem> el;                    // the page's COO elements
     std::vector<int64_t> run0;               // per run: its first element in el (sorted by row)
+    std::vector<int64_t> cur;                // per run: next free element slot
     std::vector<int32_t> idx;                // per slice: element index of (lane, step)
     for (int64_t p = lo; p < hi; p++) {
-      cd.clear(); el.clear();
-      for (int64_t i = pb[p]; i < pb[p + 1]; i++) {
-        if (c.type[i] != CBSPMV_FMT_COO) { cd.push_back(i); continue; }
-        const uint8_t *cb = coord(i);
-        for (int e = 0; e < c.nnzb[i]; e++) el.push_back(Elem{(uint32_t)c.br[i] * 16u + (cb[e] & 15u), i, e});
-      }
-      // rows ascending; a row's elements in slot order, then canonical order (stable)
-      std::stable_sort(el.begin(), el.end(), [](const Elem &a, const Elem &b) { return a.row < b.row; });
+      cd.clear();
       page_layout(p, L);
       const int64_t nruns = (int64_t)L.rows.size(), Pn = (int64_t)L.pcs.size();
       const int64_t ns = ceil_div(Pn, kSliceLanes);
       run0.assign((size_t)nruns + 1, 0);
       for (int64_t r = 0; r < nruns; r++) run0[r + 1] = run0[r] + L.cnt[r];
+      // the page's COO elements by run (rows ascending; a row's elements in slot order, then
+      // canonical order): a counting sort on the run index (binary search in the run rows)
+      el.resize((size_t)run0[nruns]);
+      cur.assign(run0.begin(), run0.end() - 1);
+      for (int64_t i = pb[p]; i < pb[p + 1]; i++) {
+        if (c.type[i] != CBSPMV_FMT_COO) { cd.push_back(i); continue; }
+        const uint8_t *cb = coord(i);
+        const uint32_t r0 = (uint32_t)c.br[i] * 16u;
+        const int64_t rb = std::lower_bound(L.rows.begin(), L.rows.end(), r0) - L.rows.begin();
+        for (int e = 0; e < c.nnzb[i]; e++) {
+          const uint32_t row = r0 + (cb[e] & 15u);
+          int64_t r = rb;
+          while (L.rows[(size_t)r] != row) r++;  // the block row's runs are consecutive, ascending
+          el[(size_t)cur[(size_t)r]++] = Elem{row, i, e};
+        }
+      }
 
       const int64_t nitems = (int64_t)cd.size() + ns;
       const int64_t desc0 = kPageHeader;
