@@ -73,6 +73,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// consumer / x-warp wait: optionally back off between probes (fewer issued spin instructions)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(bar, parity)) {
+    if (ns) __nanosleep(ns);
+  }
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -316,6 +322,7 @@ struct KParams {
   int xwarps;  // X x warps (X <= G; 0 for aggregated matrices)
   const uint32_t *hot;  // hot x columns (shared x cache), n_hot of them
   int n_hot;
+  uint32_t sleep_ns;    // consumer / x-warp back-off between mbarrier probes (0: none)
   Dbg dbg;
 };
 
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     int s = k;
     uint32_t parity = 0;
     for (uint32_t li = (uint32_t)k; dyn || li < npl; li += (uint32_t)X) {
-      mbar_wait(&full[s], parity);
+      mbar_wait_sleep(&full[s], parity, P.sleep_ns);
       const uint8_t *page = ring + (size_t)s * P.stage;
       if (reinterpret_cast<const uint32_t *>(page)[0] == cb::kEndItems) break;
       if (!(dbg.skip() & 2)) tile_page<V>(page, x, P, lane, pol);
@@ -510,11 +517,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   uint32_t parity = 0;
   int kc = wg;  // this warp's first item of the group's next page (items continue across pages)
   for (uint32_t li = (uint32_t)grp; dyn || li < npl; li += (uint32_t)G) {
-    mbar_wait(&full[s], parity);
+    mbar_wait_sleep(&full[s], parity, P.sleep_ns);
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t nitems = reinterpret_cast<const uint32_t *>(page)[0];
     if (dyn && nitems == cb::kEndItems) break;  // this group's end marker (nothing to release)
-    if (!P.agg) mbar_wait(&xrdy[s], parity);
+    if (!P.agg) mbar_wait_sleep(&xrdy[s], parity, P.sleep_ns);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
     const int n = (dbg.skip() & 4) ? 0 : (int)nitems;
     const int ncd = (int)reinterpret_cast<const uint32_t *>(page)[1];
@@ -686,6 +693,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
   const int str_env = env_int("CBSPMV_STRIDED_PAGES", -1);
   dev->strided = dev->dynamic ? 0 : std::max(0, str_env);
   dev->dbg_skip = env_int("CBSPMV_DEBUG_SKIP", 0);
+  dev->sleep_ns = (uint32_t)std::max(0, env_int("CBSPMV_WAIT_SLEEP_NS", 0));
   return CBSPMV_OK;
 }
 
@@ -708,7 +716,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     }
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.claim_chunk,
               ctr ? 0 : dev.strided, dev.m, sumsq, dev.page_cap, dev.nstage, dev.groups, dev.gwarps, dev.agg,
-              !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps, dev.d_hot, dev.n_hot,
+              !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps, dev.d_hot, dev.n_hot, dev.sleep_ns,
               Dbg{dev.dbg_skip}};
     const int smem = smem_bytes(dev);
     const void *fn = select_kernel(dev.dtype, sumsq != nullptr);

@@ -3,7 +3,7 @@
 # (run here, on the CPU box, after the GPU call):  bash tools/make_profiles.sh r2
 tag=${1:-r2}
 set -e
-for c in clustered rmat laplace; do
+for c in clustered rmat laplace uniform; do
   rep=gpurun_out/prof_$c.ncu-rep
   [ -f $rep ] || continue
   {
@@ -23,7 +23,7 @@ python tools/ncu_metrics_summary.py gpurun_out > profiles/${tag}_ncu_metrics.txt
 python - <<PY
 import json, subprocess, csv
 out = {}
-for c in ("clustered", "rmat", "laplace"):
+for c in ("clustered", "rmat", "laplace"):  # uniform: all panels, tools/ncu_uniform_traffic.sh
     raw = subprocess.run(["ncu", "-i", f"gpurun_out/prof_{c}.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     if len(rows) < 3:
@@ -33,6 +33,14 @@ for c in ("clustered", "rmat", "laplace"):
         i = h.index(k)
         return float(v[i].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u[i]]
     out[f"{c}_f64"] = g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
+import os
+if os.path.exists("gpurun_out/ncu_uniform_traffic.csv"):  # one whole SpMV = P panel launches
+    rows = list(csv.reader(l for l in open("gpurun_out/ncu_uniform_traffic.csv") if l.startswith('"')))
+    h = rows[0]
+    mi, ui, vi = h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    out["uniform_f64"] = sum(float(r[vi].replace(",", "")) * scale[r[ui]] for r in rows[1:]
+                             if r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
 print(out)
 PY

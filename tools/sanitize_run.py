@@ -31,6 +31,22 @@ for env in ({"CBSPMV_PAGE_BYTES": "4096", "CBSPMV_DYNAMIC_PAGES": "1"},
             cb.destroy(h)
     for k in env:
         del os.environ[k]
+# row-run slices with a forced hot x cache (full and 32 columns), host- and device-filled
+for env in ({"CBSPMV_HOT_MIN_PCT": "0"}, {"CBSPMV_HOT_MIN_PCT": "0", "CBSPMV_HOT_BYTES": "256", "CBSPMV_RUN_MAX": "3"}):
+    os.environ.update(env)
+    A = synth.rmat(12, 16, 3)
+    for dt in ("f64", "f32"):
+        for dbuild in (0, 1):
+            tdt = torch.float64 if dt == "f64" else torch.float32
+            h = cb.build(A, dtype=dt, device=0, device_build=dbuild)
+            assert h.info["n_hot"] > 0
+            x = torch.from_numpy(synth.vector(A.n, 0, 1)).to("cuda:0", tdt)
+            y = torch.empty(A.m, dtype=tdt, device="cuda:0")
+            cb.spmv(h, x, y)
+            torch.cuda.synchronize()
+            cb.destroy(h)
+    for k in env:
+        del os.environ[k]
 for A, opts in cases:
     for dt in ("f64", "f32"):
         tdt = torch.float64 if dt == "f64" else torch.float32
