@@ -108,6 +108,20 @@ struct Dbg {
   int skip_;
   __device__ __forceinline__ int skip() const { return CBSPMV_ABLATION ? skip_ : 0; }
 };
+// Bounds-checking debug build (-DCBSPMV_CHECK=1, tools/build_variant.sh; compute-sanitizer is not
+// available on the B200 pool): every page offset, slice element index, column, hot slot and row
+// the kernel derives from the stream is checked, and a violation traps (the launch fails with an
+// illegal-instruction error instead of reading or writing out of bounds).  Folds away otherwise.
+#ifndef CBSPMV_CHECK
+#define CBSPMV_CHECK 0
+#endif
+#define CB_CHECK(cond)                                  \
+  do {                                                  \
+    if (CBSPMV_CHECK && !(cond)) {                      \
+      printf("cbspmv check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
+      __trap();                                         \
+    }                                                   \
+  } while (0)
 
 template <typename V>
 __device__ __forceinline__ void red_add(V *p, V v, Dbg dbg) {
@@ -166,9 +180,16 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
 // piece (Alg. 3's atomicAdd).  B slices (items da0, da0 + dstride, ...) advance together so B
 // gathers per lane are in flight.  An element whose column carries kHotBit reads its x from the
 // CTA's shared copy of the hot x columns (hotx: its shared address).
+struct Bounds {  // for the CBSPMV_CHECK build
+  uint32_t stage;  // bytes of a stage (page + x area)
+  int64_t m, n;
+  int n_hot;
+};
+
 template <typename M, typename V, bool SCALED, int B>
 __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t dstride, const V *__restrict__ x,
-                                           uint32_t hotx, V *__restrict__ y, V scale, int lane, uint64_t pol, Dbg dbg) {
+                                           uint32_t hotx, V *__restrict__ y, V scale, int lane, uint64_t pol, Dbg dbg,
+                                           const Bounds &bd) {
   uint32_t cv[B], off[B], row[B];  // cv: cols offset | vals offset << 16 (page-relative)
   int len[B];
   V acc[B];
@@ -177,6 +198,9 @@ __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t d
   for (int b = 0; b < B; b++) {
     const uint4 d = lds_v4(da0 + (uint32_t)b * dstride);
     const uint32_t nl = (d.x >> 16) & 0xFF, tab = pg + (d.x & 0xFFFFu);
+    CB_CHECK((d.w & 3) == CBSPMV_FMT_COO && nl >= 1 && nl <= 32 && (d.x >> 24) >= 1);
+    CB_CHECK((d.x & 0xFFFFu) + 5 * nl <= bd.stage && (d.y & 0xFFFFu) + 4 * d.z <= bd.stage &&
+             (d.y >> 16) + sizeof(M) * d.z <= bd.stage);
     const bool in = (uint32_t)lane < nl;
     len[b] = in ? (int)lds_u8(tab + 4 * nl + lane) : 0;
     row[b] = in ? lds_u32(tab + 4 * lane) : 0;
@@ -197,6 +221,10 @@ __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t d
       const unsigned act = __ballot_sync(kFull, on[b]);
       ix[b] = off[b] + (uint32_t)__popc(act & below);
       off[b] += (uint32_t)__popc(act);
+      if (CBSPMV_CHECK && on[b]) {
+        const uint4 d = lds_v4(da0 + (uint32_t)b * dstride);
+        CB_CHECK(ix[b] < d.z && (uint32_t)len[b] <= (d.x >> 24));
+      }
     }
 #pragma unroll
     for (int b = 0; b < B; b++) c[b] = on[b] ? lds_u32(pg + (cv[b] & 0xFFFFu) + 4u * ix[b]) : 0u;
@@ -204,6 +232,7 @@ __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t d
 #pragma unroll
     for (int b = 0; b < B; b++) {
       const bool hot = (c[b] & cb::kHotBit) != 0;
+      CB_CHECK(!on[b] || (hot ? (int)(c[b] & ~cb::kHotBit) < bd.n_hot : (int64_t)c[b] < bd.n));
       V g = V(0), h = V(0);
       if (dbg.skip() & 2) g = V(1) + V(c[b] & 1);
       else if (on[b] && !hot) g = ldg_x(x + c[b], pol);
@@ -217,6 +246,7 @@ __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t d
 #pragma unroll
   for (int b = 0; b < B; b++) {
     if (len[b] > 0) {
+      CB_CHECK((int64_t)row[b] < bd.m);
       V r = acc[b];
       if constexpr (SCALED) r *= scale;
       red_add(y + row[b], r, dbg);
@@ -311,7 +341,7 @@ struct KParams {
   uint32_t n_pages;
   uint32_t claim_chunk;  // pages per dynamic claim
   int strided;           // static: K > 0 -> CTA g takes runs of K pages g, g + grid, ... (0: contiguous)
-  int64_t m;
+  int64_t m, n;
   const double *sumsq;
   int stage;   // bytes per stage: page + its x area
   int nstage;  // S
@@ -436,6 +466,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       auto load_page = [&](uint32_t p) {
         const uint64_t off = P.page_off[p];
         const uint32_t bytes = (uint32_t)(P.page_off[p + 1] - off);
+        CB_CHECK(p < P.n_pages && bytes >= 16 && bytes % 16 == 0 && bytes <= (uint32_t)P.stage);
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(ring + (size_t)s * P.stage, P.stream + off, bytes, &full[s], pol);
         advance();
@@ -512,6 +543,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
   }
   const uint32_t hota = smem_addr(hotx);
+  const Bounds bd{(uint32_t)P.stage, P.m, P.n, P.n_hot};
   const int grp = cw / W, wg = cw - grp * W;
   int s = grp;
   uint32_t parity = 0;
@@ -525,10 +557,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
     const int n = (dbg.skip() & 4) ? 0 : (int)nitems;
     const int ncd = (int)reinterpret_cast<const uint32_t *>(page)[1];
+    CB_CHECK(nitems >= 1 && cb::kPageHeader + 16ull * nitems <= (uint64_t)P.stage && ncd <= (int)nitems);
     int k = kc;
     // CSR / DENSE items first (the page lists them before the chunks)
     for (; k < ncd && k < n; k += W) {
       const uint4 d = descs[k];
+      if (CBSPMV_CHECK) {  // CSR / DENSE item: record, restore entries / x tile inside the stage, rows < m
+        const uint32_t nz = ((d.w >> 8) & 0xFF) + 1, nc = (d.w >> 2) & 31;
+        const uint32_t rec = (d.w & 3) == CBSPMV_FMT_CSR ? (d.z >> 16) + (uint32_t)sizeof(M) * nz
+                                                          : (d.z >> 16) + (uint32_t)sizeof(M) * 256;
+        CB_CHECK(((d.w & 3) == CBSPMV_FMT_CSR || (d.w & 3) == CBSPMV_FMT_DENSE) && nc <= 16 && rec <= (uint32_t)P.stage &&
+                 (int64_t)d.x < P.m);
+        CB_CHECK(P.agg ? d.y + 4 * nc <= (uint32_t)P.stage : ((int64_t)d.y < P.n && (d.w >> 16) + 16 * sizeof(V) <= (uint32_t)P.stage));
+        if (P.agg && lane < (int)nc) CB_CHECK((int64_t)reinterpret_cast<const uint32_t *>(page + d.y)[lane] < P.n);
+      }
       const V *xt = P.agg ? agg_tile<V>(page, d, x, wscratch, lane, xpol)
                           : reinterpret_cast<const V *>(page + (d.w >> 16));
       if ((d.w & 3) == CBSPMV_FMT_CSR) csr_path<M, V, SCALED>(page, d, xt, scale, y, lane, dbg);
@@ -537,13 +579,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     // COO slices, four at a time: the four slices' element loads and x gathers in flight together
     const uint32_t pg = smem_addr(page), dsc = pg + cb::kPageHeader, dW = 16u * (uint32_t)W;
     for (; k + 3 * W < n; k += 4 * W)
-      coo_slices<M, V, SCALED, 4>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg);
+      coo_slices<M, V, SCALED, 4>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
     if (k + W < n) {
-      coo_slices<M, V, SCALED, 2>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg);
+      coo_slices<M, V, SCALED, 2>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
       k += 2 * W;
     }
     if (k < n) {
-      coo_slices<M, V, SCALED, 1>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg);
+      coo_slices<M, V, SCALED, 1>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
       k += W;
     }
     if (n != (int)nitems) k += ((int)nitems - k + W - 1) / W * W;  // ablation skipped the items
@@ -715,7 +757,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
       ctr = dev.d_page_ctr + 2 * (slot % cb::kCtrSlots);
     }
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.claim_chunk,
-              ctr ? 0 : dev.strided, dev.m, sumsq, dev.page_cap, dev.nstage, dev.groups, dev.gwarps, dev.agg,
+              ctr ? 0 : dev.strided, dev.m, dev.n, sumsq, dev.page_cap, dev.nstage, dev.groups, dev.gwarps, dev.agg,
               !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps, dev.d_hot, dev.n_hot, dev.sleep_ns,
               Dbg{dev.dbg_skip}};
     const int smem = smem_bytes(dev);
