@@ -8,7 +8,7 @@ Default workload: BASELINE configs[3] (block-clustered, 2^22 rows, ~407M nnz,
 fp64) — the large synthetic matrix whose HBM roofline the metric asks for and
 the one config exercising all three warp paths (DESIGN.md §6 explains the
 choice); R-MAT (configs[2]) and the Laplacian (configs[1]) are measured with the
-same protocol in the same run and reported under "config.also".
+same protocol in the same run and reported under "detail.also".
 
 A step is one y := A·x over the whole (row-sharded) matrix through the C ABI
 (cbspmv_spmv: zero y + the persistent SpMV kernel).  Inputs already resident in
@@ -41,7 +41,7 @@ WORKLOAD = {
     "rmat": "BASELINE configs[2]: synthetic R-MAT scale 23, edge factor 16 (8,388,608 rows, ~131M nnz after dedup)",
     "clustered": "BASELINE configs[3]: synthetic block-clustered 2^22 rows, ~407M nnz, dense/CSR/COO mix",
     "laplace": "BASELINE configs[1]: 5-point Laplacian on a 1000x1000 grid (1M rows, 4,996,000 nnz)",
-    "uniform": "BASELINE configs[4] (row shard sizes): uniform random 2^25 rows x 50/row",
+    "uniform": "BASELINE configs[4]: power iteration on uniform random 2^25 x 2^25, 50 nnz/row",
 }
 
 
@@ -106,14 +106,14 @@ def make_matrix(config: str, rank: int, world: int):
     """This rank's row shard, generated alone ("each rank generates and builds only
     its rows"): the cut comes from per-row counts (synth.row_counts, no matrix materialised;
     rows split by nnz at block-row boundaries, equal shards for the uniform matrix), then the
-    counter-based generator produces rows [r0, r1) only.  Returns (shard, (r0, r1), total nnz);
-    the total is all-reduced by the caller when world > 1."""
+    counter-based generator produces rows [r0, r1) only.  Returns (shard, (r0, r1), total nnz,
+    total rows); the nnz total is all-reduced by the caller when world > 1."""
     import numpy as np
     import synth
     from paper_2605_18515_b200 import dist
     if world == 1:
         A = synth.make(config)
-        return A, (0, A.m), A.nnz
+        return A, (0, A.m), A.nnz, A.m
     counts = synth.row_counts(config)
     if config == "uniform":
         cuts = dist.equal_bounds(len(counts), world)
@@ -123,7 +123,7 @@ def make_matrix(config: str, rank: int, world: int):
         cuts = dist.shard_bounds(rp, world)
     r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
     S = synth.make(config, r0, r1)
-    return S, (r0, r1), None
+    return S, (r0, r1), None, len(counts)
 
 
 def peaks():
@@ -226,7 +226,7 @@ def run_cb(args, rank: int, world: int, local_rank: int):
             tdist.barrier()
 
     t0 = time.perf_counter()
-    A, (r0, r1), nnz_total = make_matrix(args.config, rank, world)
+    A, (r0, r1), nnz_total, m_total = make_matrix(args.config, rank, world)
     gen_s = time.perf_counter() - t0
     if nnz_total is None:
         nnz_total = int(allreduce(np.array([A.nnz], np.int64))[0])
@@ -326,9 +326,10 @@ def run_cb(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded generators, synth/)",
-            "config": {
-                "workload": WORKLOAD[args.config], "name": args.config, "m": int(info["m"]) if world == 1 else None,
-                "nnz": int(nnz_total), "agg": int(info["agg"]), "blocks": int(info["nb"]),
+            # config: the workload alone, identical to the reference arm's; run details under "detail"
+            "config": {"workload": WORKLOAD[args.config], "name": args.config, "m": int(m_total), "nnz": int(nnz_total)},
+            "detail": {
+                "agg": int(info["agg"]), "blocks": int(info["nb"]),
                 "fmt_count_coo_csr_dense": list(info["fmt_count"]), "parallelism": f"row-shard x{world}",
                 **({"shared_gpu_test": True} if shared_gpu_test() else {}),
                 "l2": "inputs larger than L2 (matrix stream %.2f GB vs 126 MB L2); cold_l2_ms flushes 512 MB "
@@ -419,14 +420,14 @@ def run_power(args, rank, world, local_rank):
     if shared_gpu_test() and world > 1 and args.exchange != "fused":
         raise SystemExit("CBSPMV_BENCH_SHARED_GPU runs the power iteration with --exchange fused only (gloo host collectives)")
     t0 = time.perf_counter()
-    A, (r0, r1), nnz_total = make_matrix("uniform", rank, world)
+    A, (r0, r1), nnz_total, m_total = make_matrix("uniform", rank, world)
     gen_s = time.perf_counter() - t0
     if nnz_total is None:
         nnz_total = int(_allreduce_np(np.array([A.nnz], np.int64), cdev, world)[0])
     agg = dist.global_agg(A, lambda a: _allreduce_np(a, cdev, world), dtype=args.dtype) if world > 1 else -1
     # column panels: the auto count on one GPU (x slices L2-resident); with N ranks a multiple
     # of N so panel cuts fall on the x owners' boundaries (NEXT-1 (i) overlap)
-    panels = 0 if world == 1 else world * max(1, -(-11 // world))
+    panels = 0 if world == 1 else world * max(1, -(-6 // world))  # 1 GPU: the auto count (6)
     h = cb.build(A, dtype=args.dtype, device=local_rank, agg_mode=agg, keep_host=0, col_panels=panels)
     info = h.info
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
@@ -515,8 +516,8 @@ def run_power(args, rank, world, local_rank):
             "metric": METRIC, "value": 2.0 * nnz_total / (ms_max * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded generators, synth/)",
-            "config": {"workload": "BASELINE configs[4]: power iteration on uniform 2^25 x 2^25, 50 nnz/row",
-                       "name": "uniform", "nnz": int(nnz_total), "rows_per_rank": int(A.m), "agg": int(info["agg"]),
+            "config": {"workload": WORKLOAD["uniform"], "name": "uniform", "m": int(m_total), "nnz": int(nnz_total)},
+            "detail": {"rows_per_rank": int(A.m), "agg": int(info["agg"]),
                        "lambda": lam, "gen_s": gen_s, "build_s": info["build_seconds"],
                        "n_panels": int(info["n_panels"]), "gather_floor": gather_floor(info, kernel_ms),
                        "step_split": split, "rows_per_rank_range": [int(r0), int(r1)],

@@ -256,6 +256,7 @@ struct CbDevice : CbShape {
   uint32_t claim_chunk = 8;  // pages per dynamic claim
   int dbg_skip = 0;          // ablation build only (CBSPMV_DEBUG_SKIP)
   uint32_t sleep_ns = 0;     // consumer / x-warp back-off between mbarrier probes (CBSPMV_WAIT_SLEEP_NS)
+  int pdl = 1;               // launch the SpMV dependent on the y-zeroing kernel (CBSPMV_PDL=0: off)
   const uint8_t *d_stream = nullptr;
   const uint64_t *d_page_off = nullptr;
   const uint32_t *d_cta_page = nullptr;  // grid + 1 page boundaries per persistent CTA

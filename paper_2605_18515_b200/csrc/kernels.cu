@@ -544,6 +544,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   }
   const uint32_t hota = smem_addr(hotx);
   const Bounds bd{(uint32_t)P.stage, P.m, P.n, P.n_hot};
+  // launched dependent on the y-zeroing kernel (PDL): no RED before that grid has finished; a
+  // no-op for a normal launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int grp = cw / W, wg = cw - grp * W;
   int s = grp;
   uint32_t parity = 0;
@@ -597,8 +600,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   }
 }
 
+// Programmatic dependent launch: the SpMV kernel that follows may start (barrier set-up, the
+// producer's first page copies, the hot x copy) while y is being zeroed; its consumers wait for
+// this grid (griddepcontrol.wait) before their first RED.
 template <typename V>
 __global__ void cb_zero_kernel(V *__restrict__ y, int64_t m) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = V(0);
 }
@@ -736,6 +743,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
   dev->strided = dev->dynamic ? 0 : std::max(0, str_env);
   dev->dbg_skip = env_int("CBSPMV_DEBUG_SKIP", 0);
   dev->sleep_ns = (uint32_t)std::max(0, env_int("CBSPMV_WAIT_SLEEP_NS", 0));
+  dev->pdl = env_int("CBSPMV_PDL", 1) != 0;
   return CBSPMV_OK;
 }
 
@@ -764,7 +772,17 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     const void *fn = select_kernel(dev.dtype, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
     const int threads = 32 * (1 + dev.xwarps + dev.groups * dev.gwarps);
-    cudaError_t e = cudaLaunchKernel(fn, dim3(dev.grid), dim3(threads), args, (size_t)smem, st);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(dev.grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the zeroing kernel
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (zero_y && dev.m > 0 && dev.pdl) ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return cuda_fail(e, "spmv kernel launch", err);
   }
   cudaError_t e = cudaGetLastError();

@@ -168,7 +168,7 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
     int64_t n_coo = 0;
     for (int64_t i = 0; i < c.nb; i++) n_coo += c.type[i] == CBSPMV_FMT_COO ? c.nnzb[i] : 0;
     const bool force = so.hot_min_pct == 0;
-    if (H > 0 && n_coo > 0 && c.n <= (int64_t)1 << 28 && (force || n_coo >= 4 * 148 * H)) {
+    if (H > 0 && n_coo > 0 && c.n <= (int64_t)1 << 27 && (force || n_coo >= 4 * 148 * H)) {  // count array <= 512 MB
       // estimate on every 251st COO block first (uniform-like matrices stop here)
       std::vector<uint32_t> samp;
       for (int64_t i = 0; i < c.nb; i += 251)
