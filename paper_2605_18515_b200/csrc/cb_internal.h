@@ -257,6 +257,7 @@ struct CbDevice : CbShape {
   int dbg_skip = 0;          // ablation build only (CBSPMV_DEBUG_SKIP)
   uint32_t sleep_ns = 0;     // consumer / x-warp back-off between mbarrier probes (CBSPMV_WAIT_SLEEP_NS)
   int pdl = 1;               // launch the SpMV dependent on the y-zeroing kernel (CBSPMV_PDL=0: off)
+  int csr_pair = 0;          // two CSR blocks per warp, one lane per row (non-aggregated; CBSPMV_CSR_PAIR)
   const uint8_t *d_stream = nullptr;
   const uint64_t *d_page_off = nullptr;
   const uint32_t *d_cta_page = nullptr;  // grid + 1 page boundaries per persistent CTA

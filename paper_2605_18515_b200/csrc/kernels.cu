@@ -294,6 +294,32 @@ __device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, co
   if (h == 0 && hi > lo) red_add(y + d.x + r, acc, dbg);
 }
 
+// Two CSR blocks of non-aggregated matrices at once: lanes 0-15 take rows 0-15 of block A, lanes
+// 16-31 those of block B, one lane per row (no shuffle; one RED instruction for both blocks).
+template <typename M, typename V, bool SCALED>
+__device__ __forceinline__ void csr_pair(const uint8_t *page, const uint4 &dA, const uint4 &dB, V scale,
+                                         V *__restrict__ y, int lane, Dbg dbg) {
+  const uint4 d = lane < 16 ? dA : dB;
+  const V *xt = reinterpret_cast<const V *>(page + (d.w >> 16));
+  const uint8_t *body = page + (d.z & 0xFFFFu);
+  const uint8_t *cols = body + 17;
+  const M *vals = reinterpret_cast<const M *>(page + (d.z >> 16));
+  const int nnz = (int)((d.w >> 8) & 0xFF) + 1;
+  const int r = lane & 15;
+  const int lo = body[r];
+  const int hi = r < 15 ? (int)body[r + 1] : nnz;  // row_ptr[16] = nnz mod 256 (R-8)
+  V a0 = V(0), a1 = V(0);
+  int e = lo;
+  for (; e + 1 < hi; e += 2) {
+    a0 = fma(V(vals[e]), xt[cols[e]], a0);
+    a1 = fma(V(vals[e + 1]), xt[cols[e + 1]], a1);
+  }
+  if (e < hi) a0 = fma(V(vals[e]), xt[cols[e]], a0);
+  V acc = a0 + a1;
+  if constexpr (SCALED) acc *= scale;
+  if (hi > lo) red_add(y + d.x + r, acc, dbg);
+}
+
 // DENSE (Alg. 4): the device record stores the 256 values in lane-major 16-byte pairs (pair
 // q*32 + l holds A[l % 16][(l / 16) * 8 + 2q + {0, 1}]), so lane l owns row l % 16, columns
 // 8*(l/16) .. +7: 4 conflict-free 16-byte shared loads (8-byte for fp32), 8 FMAs against the
@@ -353,6 +379,7 @@ struct KParams {
   const uint32_t *hot;  // hot x columns (shared x cache), n_hot of them
   int n_hot;
   uint32_t sleep_ns;    // consumer / x-warp back-off between mbarrier probes (0: none)
+  int csr_pair;         // non-aggregated: a warp takes two CSR blocks at once (one lane per row)
   Dbg dbg;
 };
 
@@ -565,6 +592,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     // CSR / DENSE items first (the page lists them before the chunks)
     for (; k < ncd && k < n; k += W) {
       const uint4 d = descs[k];
+      if (P.csr_pair && (d.w & 3) == CBSPMV_FMT_CSR && k + W < ncd && k + W < n &&
+          (descs[k + W].w & 3) == CBSPMV_FMT_CSR) {  // this warp's next item is CSR too: both at once
+        if (CBSPMV_CHECK) {
+          const uint4 e = descs[k + W];
+          CB_CHECK((d.z >> 16) + (uint32_t)sizeof(M) * (((d.w >> 8) & 0xFF) + 1) <= (uint32_t)P.stage &&
+                   (e.z >> 16) + (uint32_t)sizeof(M) * (((e.w >> 8) & 0xFF) + 1) <= (uint32_t)P.stage);
+          CB_CHECK((int64_t)d.x < P.m && (int64_t)e.x < P.m && (int64_t)d.y < P.n && (int64_t)e.y < P.n &&
+                   (d.w >> 16) + 16 * sizeof(V) <= (uint32_t)P.stage && (e.w >> 16) + 16 * sizeof(V) <= (uint32_t)P.stage);
+        }
+        csr_pair<M, V, SCALED>(page, d, descs[k + W], scale, y, lane, dbg);
+        k += W;
+        continue;
+      }
       if (CBSPMV_CHECK) {  // CSR / DENSE item: record, restore entries / x tile inside the stage, rows < m
         const uint32_t nz = ((d.w >> 8) & 0xFF) + 1, nc = (d.w >> 2) & 31;
         const uint32_t rec = (d.w & 3) == CBSPMV_FMT_CSR ? (d.z >> 16) + (uint32_t)sizeof(M) * nz
@@ -744,6 +784,9 @@ int cb_configure(CbDevice *dev, std::string *err) {
   dev->dbg_skip = env_int("CBSPMV_DEBUG_SKIP", 0);
   dev->sleep_ns = (uint32_t)std::max(0, env_int("CBSPMV_WAIT_SLEEP_NS", 0));
   dev->pdl = env_int("CBSPMV_PDL", 1) != 0;
+  // paired CSR blocks (one lane per row; fewer instructions): clustered fp32 0.498 -> 0.444 ms,
+  // mixed 0.629 -> 0.571, fp64 0.754 -> 0.747 (4 interleaved A/B pairs; 400-launch sustained 0.836 -> 0.814)
+  dev->csr_pair = env_int("CBSPMV_CSR_PAIR", 1) != 0;
   return CBSPMV_OK;
 }
 
@@ -767,7 +810,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.claim_chunk,
               ctr ? 0 : dev.strided, dev.m, dev.n, sumsq, dev.page_cap, dev.nstage, dev.groups, dev.gwarps, dev.agg,
               !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps, dev.d_hot, dev.n_hot, dev.sleep_ns,
-              Dbg{dev.dbg_skip}};
+              dev.csr_pair && !dev.agg, Dbg{dev.dbg_skip}};
     const int smem = smem_bytes(dev);
     const void *fn = select_kernel(dev.dtype, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};

@@ -727,6 +727,7 @@ _SHAPES = [
     {"CBSPMV_STAGES": "30", "CBSPMV_GROUPS": "5", "CBSPMV_GROUP_WARPS": "5", "CBSPMV_XWARPS": "5"},
     {"CBSPMV_STAGES": "16", "CBSPMV_GROUPS": "4", "CBSPMV_GROUP_WARPS": "6", "CBSPMV_XWARPS": "4"},
     {"CBSPMV_PAGE_BYTES": "4096"}, {"CBSPMV_WAIT_SLEEP_NS": "128"}, {"CBSPMV_PDL": "0"},
+    {"CBSPMV_CSR_PAIR": "1"}, {"CBSPMV_CSR_PAIR": "0"},
 ]
 
 
