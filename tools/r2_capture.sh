@@ -16,8 +16,10 @@ done
 for dt in f32 f32f64; do
   timeout 900 python bench.py --dtype $dt --steps 100 --warmup 5 --no-cpu-baseline --also rmat > gpurun_out/bench_clustered_$dt.log 2>&1; echo bench_$dt=$?
 done
-timeout 1200 python tools/ablation.py --configs clustered,rmat,laplace > gpurun_out/ablation.jsonl 2> gpurun_out/ablation.err; echo ablation_rc=$?
-timeout 1500 python tools/build_timing.py --out gpurun_out/build_timing.json > gpurun_out/build_timing.log 2>&1; echo timing_rc=$?
+timeout 1800 python tools/ablation.py --configs clustered,rmat,laplace,uniform > gpurun_out/ablation.jsonl 2> gpurun_out/ablation.err; echo ablation_rc=$?
+if [ "${SKIP_TIMING:-0}" != "1" ]; then
+  timeout 1500 python tools/build_timing.py --out gpurun_out/build_timing.json > gpurun_out/build_timing.log 2>&1; echo timing_rc=$?
+fi
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv \
    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --also "" > gpurun_out/bench_under_ncu.log 2>&1; echo launch_rc=$?
 for c in clustered rmat laplace; do
@@ -25,3 +27,4 @@ for c in clustered rmat laplace; do
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cb_spmv_kernel -s 12 -c 1 -f -o gpurun_out/prof_uniform python tools/prof_kernel.py --config uniform --launches 3 > gpurun_out/ncu_uniform.log 2>&1; echo prof_uniform_rc=$?
 bash tools/ncu_metrics.sh > gpurun_out/ncu_metrics.log 2>&1; echo metrics_rc=$?
+bash tools/ncu_uniform_traffic.sh
