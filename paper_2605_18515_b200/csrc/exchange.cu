@@ -77,7 +77,23 @@ __global__ void __launch_bounds__(kPubThreads) xchg_publish_kernel(PubArgs A, in
   uint8_t *own = A.peer[A.rank];
   const V *y = reinterpret_cast<const V *>(own + xoff_b) + r0;
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  // 16-byte loads and peer stores (fewer, larger NVLink writes) when the slice is 16-byte aligned
+  // (row shards start at block-row boundaries); the tail and unaligned slices element by element
+  constexpr int kPer = 16 / (int)sizeof(V);
+  const bool vec = ((uintptr_t)y % 16) == 0 && ((uintptr_t)(xoff_b + r0 * (int64_t)sizeof(V)) % 16) == 0;
+  const int64_t nvec = vec ? len / kPer : 0;
+  for (int64_t i = tid; i < nvec; i += nth) {
+    const uint4 u = reinterpret_cast<const uint4 *>(y)[i];
+    V v[kPer];
+    memcpy(v, &u, 16);
+#pragma unroll
+    for (int j = 0; j < kPer; j++) acc = fma((double)v[j], (double)v[j], acc);
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; q++)
+      if (q < A.world && q != A.rank) reinterpret_cast<uint4 *>(A.peer[q] + xoff_b + r0 * (int64_t)sizeof(V))[i] = u;
+  }
+  for (int64_t i = nvec * kPer + tid; i < len; i += nth) {
     const V v = y[i];
     acc = fma((double)v, (double)v, acc);
 #pragma unroll

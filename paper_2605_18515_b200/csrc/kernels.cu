@@ -186,10 +186,11 @@ struct Bounds {  // for the CBSPMV_CHECK build
   int n_hot;
 };
 
-template <typename M, typename V, bool SCALED, int B>
+template <typename M, typename V, bool SCALED, int B, int U>
 __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t dstride, const V *__restrict__ x,
                                            uint32_t hotx, V *__restrict__ y, V scale, int lane, uint64_t pol, Dbg dbg,
                                            const Bounds &bd) {
+  constexpr int N = B * U;  // elements per lane in flight: B slices x U steps
   uint32_t cv[B], off[B], row[B];  // cv: cols offset | vals offset << 16 (page-relative)
   int len[B];
   V acc[B];
@@ -210,38 +211,42 @@ __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t d
     wmax = max(wmax, (int)(d.x >> 24));
   }
   const unsigned below = (1u << lane) - 1u;
-  for (int j = 0; j < wmax; j++) {
-    // the B slices' element indices first, then their column loads, then the gathers: no shared
-    // load waits between two gathers
-    uint32_t ix[B], c[B];
-    bool on[B];
+  for (int j = 0; j < wmax; j += U) {
+    // the element indices of B slices x U steps first, then their column loads, then the
+    // gathers: no shared-load wait between two gathers
+    uint32_t ix[N], c[N];
+    bool on[N];
 #pragma unroll
-    for (int b = 0; b < B; b++) {
-      on[b] = len[b] > j;
-      const unsigned act = __ballot_sync(kFull, on[b]);
-      ix[b] = off[b] + (uint32_t)__popc(act & below);
-      off[b] += (uint32_t)__popc(act);
-      if (CBSPMV_CHECK && on[b]) {
-        const uint4 d = lds_v4(da0 + (uint32_t)b * dstride);
-        CB_CHECK(ix[b] < d.z && (uint32_t)len[b] <= (d.x >> 24));
+    for (int u = 0; u < U; u++) {
+#pragma unroll
+      for (int b = 0; b < B; b++) {
+        const int e = u * B + b;
+        on[e] = len[b] > j + u;
+        const unsigned act = __ballot_sync(kFull, on[e]);
+        ix[e] = off[b] + (uint32_t)__popc(act & below);
+        off[b] += (uint32_t)__popc(act);
+        if (CBSPMV_CHECK && on[e]) {
+          const uint4 d = lds_v4(da0 + (uint32_t)b * dstride);
+          CB_CHECK(ix[e] < d.z && (uint32_t)len[b] <= (d.x >> 24));
+        }
       }
     }
 #pragma unroll
-    for (int b = 0; b < B; b++) c[b] = on[b] ? lds_u32(pg + (cv[b] & 0xFFFFu) + 4u * ix[b]) : 0u;
-    V xv[B];
+    for (int e = 0; e < N; e++) c[e] = on[e] ? lds_u32(pg + (cv[e % B] & 0xFFFFu) + 4u * ix[e]) : 0u;
+    V xv[N];
 #pragma unroll
-    for (int b = 0; b < B; b++) {
-      const bool hot = (c[b] & cb::kHotBit) != 0;
-      CB_CHECK(!on[b] || (hot ? (int)(c[b] & ~cb::kHotBit) < bd.n_hot : (int64_t)c[b] < bd.n));
+    for (int e = 0; e < N; e++) {
+      const bool hot = (c[e] & cb::kHotBit) != 0;
+      CB_CHECK(!on[e] || (hot ? (int)(c[e] & ~cb::kHotBit) < bd.n_hot : (int64_t)c[e] < bd.n));
       V g = V(0), h = V(0);
-      if (dbg.skip() & 2) g = V(1) + V(c[b] & 1);
-      else if (on[b] && !hot) g = ldg_x(x + c[b], pol);
-      if (on[b] && hot) h = lds_val<V>(hotx + (uint32_t)sizeof(V) * (c[b] & ~cb::kHotBit));  // shared x cache
-      xv[b] = hot ? h : g;
+      if (dbg.skip() & 2) g = V(1) + V(c[e] & 1);
+      else if (on[e] && !hot) g = ldg_x(x + c[e], pol);
+      if (on[e] && hot) h = lds_val<V>(hotx + (uint32_t)sizeof(V) * (c[e] & ~cb::kHotBit));  // shared x cache
+      xv[e] = hot ? h : g;
     }
 #pragma unroll
-    for (int b = 0; b < B; b++)
-      if (on[b]) acc[b] = fma(V(lds_val<M>(pg + (cv[b] >> 16) + (uint32_t)sizeof(M) * ix[b])), xv[b], acc[b]);
+    for (int e = 0; e < N; e++)  // step order per slice (u-major): a piece is summed in sequence
+      if (on[e]) acc[e % B] = fma(V(lds_val<M>(pg + (cv[e % B] >> 16) + (uint32_t)sizeof(M) * ix[e])), xv[e], acc[e % B]);
   }
 #pragma unroll
   for (int b = 0; b < B; b++) {
@@ -621,14 +626,16 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     }
     // COO slices, four at a time: the four slices' element loads and x gathers in flight together
     const uint32_t pg = smem_addr(page), dsc = pg + cb::kPageHeader, dW = 16u * (uint32_t)W;
+    // (a warp holding fewer than four slices of the page unrolls their steps instead: always four
+    // elements per lane in flight)
     for (; k + 3 * W < n; k += 4 * W)
-      coo_slices<M, V, SCALED, 4>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
+      coo_slices<M, V, SCALED, 4, 1>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
     if (k + W < n) {
-      coo_slices<M, V, SCALED, 2>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
+      coo_slices<M, V, SCALED, 2, 2>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
       k += 2 * W;
     }
     if (k < n) {
-      coo_slices<M, V, SCALED, 1>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
+      coo_slices<M, V, SCALED, 1, 4>(pg, dsc + 16u * (uint32_t)k, dW, x, hota, y, scale, lane, xpol, dbg, bd);
       k += W;
     }
     if (n != (int)nitems) k += ((int)nitems - k + W - 1) / W * W;  // ablation skipped the items

@@ -47,11 +47,13 @@ def _reference(A, steps, dtype=torch.float64):
     return x, ss
 
 
-def _simulated_ranks(A, P, steps, dtype="f64", unequal=False):
+def _simulated_ranks(A, P, steps, dtype="f64", unequal=False, bounds=None):
     """P ranks in one process on one GPU, run step-interleaved on one stream.  unequal: the
-    shards of dist.shard_bounds (nnz cut at block-row boundaries, unequal row counts)."""
+    shards of dist.shard_bounds (nnz cut at block-row boundaries, unequal row counts); bounds:
+    explicit row ranges."""
     m_loc = A.m // P
-    bounds = [(r * m_loc, (r + 1) * m_loc) for r in range(P)]
+    if bounds is None:
+        bounds = [(r * m_loc, (r + 1) * m_loc) for r in range(P)]
     if unequal:
         cuts = cbd.shard_bounds(A.row_ptr, P)
         bounds = cbd.check_row_bounds(list(zip(cuts[:-1], cuts[1:])), A.n)
@@ -117,6 +119,24 @@ def test_fused_exchange_unequal_shards(P):
     assert len(set(ss)) == 1 and np.isclose(ss[0], ss_ref, rtol=1e-12)
     for x in xs:
         assert np.array_equal(x, xs[0]) and np.allclose(x, x_ref, rtol=1e-11, atol=1e-300)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_fused_exchange_ragged_slices(dtype):
+    """Slices whose offsets / lengths are not multiples of a 16-byte store (odd row cuts): the
+    publish kernel's unaligned and tail paths next to its 16-byte path."""
+    _ok()
+    n = 3001
+    A = synth.uniform(n, n, 30, 63, val_mode=1)
+    bounds = [(0, 1001), (1001, 2002), (2002, 3001)]  # offsets 1001 / 2002: not 16-byte aligned
+    steps = 8
+    x_ref, ss_ref = _reference(A, steps, torch.float32 if dtype == "f32" else torch.float64)
+    xs, ss = _simulated_ranks(A, 3, steps, dtype=dtype, bounds=bounds)
+    assert len(set(ss)) == 1
+    tol = 1e-5 if dtype == "f32" else 1e-12
+    assert np.isclose(ss[0], ss_ref, rtol=tol)
+    for x in xs:
+        assert np.array_equal(x, xs[0]) and np.allclose(x, x_ref, rtol=tol, atol=0)
 
 
 def test_fused_exchange_all_ones_fixed_point():
