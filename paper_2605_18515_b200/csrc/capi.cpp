@@ -495,7 +495,7 @@ static int launch_all(cbspmv_handle_t h, const void *x, void *y, const double *s
   bool first = true;
   for (const Part &p : h->parts) {
     if (p.n_pages == 0 && !(first && zero)) continue;
-    int st = cb_launch_spmv(p.dev, x, y, ss, first && zero, stream, err);
+    int st = cb_launch_spmv(p.dev, x, y, ss, first && zero, stream, err, !first);
     if (st != CBSPMV_OK) return st;
     first = false;
   }

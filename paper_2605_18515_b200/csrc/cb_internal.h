@@ -274,9 +274,10 @@ struct CbDevice : CbShape {
 int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err);
 // Grid and page assignment for this device and stream (dev's shape already planned).
 int cb_configure(CbDevice *dev, std::string *err);
-// y (+)= A·(s·x); zero_y: clear y first; sumsq: nullptr or device double (s = 1/sqrt(*sumsq)).
+// y (+)= A·(s·x); zero_y: clear y first; sumsq: nullptr or device double (s = 1/sqrt(*sumsq));
+// follows: this launch follows another panel's launch of the same SpMV on the stream (PDL overlap).
 int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *sumsq, bool zero_y,
-                   void *stream, std::string *err);
+                   void *stream, std::string *err, bool follows = false);
 int cb_launch_sumsq(const void *v, int64_t len, int dtype, double *out, void *stream, std::string *err);
 // Record msg as cbspmv_last_error() and return st (capi.cpp owns the thread-local string).
 int cb_set_error(int st, const std::string &msg);

@@ -37,7 +37,8 @@ namespace {
 
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxStages = 32;
-constexpr int kSmemHeader = 1024;  // mbarriers: full[32], xready[32], empty[32]
+constexpr int kSmemHeader = 1024;  // mbarriers: full[32], xready[32], empty[32]; the scale at 768
+constexpr int kScaleSlot = 3 * 32 * 8;
 constexpr int kAggPageBytes = 20480;  // stage bytes of aggregated matrices (the rest of the array is L1)
 constexpr unsigned kFull = 0xffffffffu;
 // End marker of dynamic page claiming: a 16-byte page header (nitems = kEndItems) copied into
@@ -188,7 +189,7 @@ struct Bounds {  // for the CBSPMV_CHECK build
 
 template <typename M, typename V, bool SCALED, int B, int U>
 __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t dstride, const V *__restrict__ x,
-                                           uint32_t hotx, V *__restrict__ y, V scale, int lane, uint64_t pol, Dbg dbg,
+                                           uint32_t hotx, V *__restrict__ y, uint32_t sc, int lane, uint64_t pol, Dbg dbg,
                                            const Bounds &bd) {
   constexpr int N = B * U;  // elements per lane in flight: B slices x U steps
   uint32_t cv[B], off[B], row[B];  // cv: cols offset | vals offset << 16 (page-relative)
@@ -253,7 +254,7 @@ __device__ __forceinline__ void coo_slices(uint32_t pg, uint32_t da0, uint32_t d
     if (len[b] > 0) {
       CB_CHECK((int64_t)row[b] < bd.m);
       V r = acc[b];
-      if constexpr (SCALED) r *= scale;
+      if constexpr (SCALED) r *= lds_val<V>(sc);  // the launch's scale, in shared memory
       red_add(y + row[b], r, dbg);
     }
   }
@@ -277,7 +278,7 @@ __device__ __forceinline__ const V *agg_tile(const uint8_t *page, const uint4 &d
 // CSR: 17 u8 row_ptr, nnz u8 local cols, pad, values; lanes 2r, 2r+1 share row r
 // ("32 threads collaboratively compute 16 y elements").
 template <typename M, typename V, bool SCALED>
-__device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, const V *xt, V scale,
+__device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, const V *xt, uint32_t sc,
                                          V *__restrict__ y, int lane, Dbg dbg) {
   const uint8_t *body = page + (d.z & 0xFFFFu);
   const uint8_t *cols = body + 17;
@@ -295,14 +296,14 @@ __device__ __forceinline__ void csr_path(const uint8_t *page, const uint4 &d, co
   if (e < hi) a0 = fma(V(vals[e]), xt[cols[e]], a0);
   V acc = a0 + a1;
   acc += __shfl_xor_sync(kFull, acc, 1);
-  if constexpr (SCALED) acc *= scale;
+  if constexpr (SCALED) acc *= lds_val<V>(sc);
   if (h == 0 && hi > lo) red_add(y + d.x + r, acc, dbg);
 }
 
 // Two CSR blocks of non-aggregated matrices at once: lanes 0-15 take rows 0-15 of block A, lanes
 // 16-31 those of block B, one lane per row (no shuffle; one RED instruction for both blocks).
 template <typename M, typename V, bool SCALED>
-__device__ __forceinline__ void csr_pair(const uint8_t *page, const uint4 &dA, const uint4 &dB, V scale,
+__device__ __forceinline__ void csr_pair(const uint8_t *page, const uint4 &dA, const uint4 &dB, uint32_t sc,
                                          V *__restrict__ y, int lane, Dbg dbg) {
   const uint4 d = lane < 16 ? dA : dB;
   const V *xt = reinterpret_cast<const V *>(page + (d.w >> 16));
@@ -321,7 +322,7 @@ __device__ __forceinline__ void csr_pair(const uint8_t *page, const uint4 &dA, c
   }
   if (e < hi) a0 = fma(V(vals[e]), xt[cols[e]], a0);
   V acc = a0 + a1;
-  if constexpr (SCALED) acc *= scale;
+  if constexpr (SCALED) acc *= lds_val<V>(sc);
   if (hi > lo) red_add(y + d.x + r, acc, dbg);
 }
 
@@ -332,7 +333,7 @@ __device__ __forceinline__ void csr_pair(const uint8_t *page, const uint4 &dA, c
 // REDs.  Absent entries are stored zeros; a non-finite x in the tile would make 0·inf poison a
 // row, so a warp whose sums are not all finite recomputes skipping the stored zeros.
 template <typename M, typename V, bool SCALED>
-__device__ __forceinline__ void dense_path(const uint8_t *page, const uint4 &d, const V *xt, V scale,
+__device__ __forceinline__ void dense_path(const uint8_t *page, const uint4 &d, const V *xt, uint32_t sc,
                                            V *__restrict__ y, int64_t m, int lane, Dbg dbg) {
   using M2 = typename Pair<M>::type;
   using V2 = typename Pair<V>::type;
@@ -359,7 +360,7 @@ __device__ __forceinline__ void dense_path(const uint8_t *page, const uint4 &d, 
     }
   }
   acc += __shfl_xor_sync(kFull, acc, 16);
-  if constexpr (SCALED) acc *= scale;
+  if constexpr (SCALED) acc *= lds_val<V>(sc);
   if (h == 0 && (int64_t)d.x + r < m) red_add(y + d.x + r, acc, dbg);
 }
 
@@ -385,6 +386,7 @@ struct KParams {
   int n_hot;
   uint32_t sleep_ns;    // consumer / x-warp back-off between mbarrier probes (0: none)
   int csr_pair;         // non-aggregated: a warp takes two CSR blocks at once (one lane per row)
+  int pdl_wait;         // launched dependent on the y-zeroing kernel: wait for it before any RED
   Dbg dbg;
 };
 
@@ -480,6 +482,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       mbar_init(&empty[s], (uint32_t)W);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if constexpr (SCALED) *reinterpret_cast<V *>(smem + kScaleSlot) = (V)(1.0 / sqrt(*P.sumsq));
   }
   __syncthreads();
 
@@ -561,8 +564,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   }
 
   // ---------------- consumers: group g takes pages g, g + G, ... (stages g, g + G, ...)
-  V scale = V(1);
-  if constexpr (SCALED) scale = (V)(1.0 / sqrt(*P.sumsq));
+  // SCALED: s = 1/sqrt(*sumsq), computed once per CTA into the mbarrier area's spare bytes (no
+  // register held through the item loops)
+  const uint32_t scale = smem_addr(smem + kScaleSlot);
   const int cw = warp - 1 - P.xwarps;
   V *wscratch = reinterpret_cast<V *>(smem + kSmemHeader + (size_t)S * P.stage) + cw * 16;
   const uint64_t xpol = policy_evict_last();
@@ -576,9 +580,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   }
   const uint32_t hota = smem_addr(hotx);
   const Bounds bd{(uint32_t)P.stage, P.m, P.n, P.n_hot};
-  // launched dependent on the y-zeroing kernel (PDL): no RED before that grid has finished; a
-  // no-op for a normal launch
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Launched dependent on the y-zeroing kernel (PDL): no RED before that grid has finished (a
+  // no-op for a normal launch).  Then this CTA lets the next launch of the same SpMV (the next
+  // column panel: REDs commute, so panels need not wait for each other) start on SMs this grid
+  // frees; y is zeroed by then.
+  if (P.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int grp = cw / W, wg = cw - grp * W;
   int s = grp;
   uint32_t parity = 0;
@@ -798,7 +805,7 @@ int cb_configure(CbDevice *dev, std::string *err) {
 }
 
 int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *sumsq, bool zero_y, void *stream,
-                   std::string *err) {
+                   std::string *err, bool follows) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (zero_y && dev.m > 0) {
     const int zb = 256;
@@ -817,7 +824,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.claim_chunk,
               ctr ? 0 : dev.strided, dev.m, dev.n, sumsq, dev.page_cap, dev.nstage, dev.groups, dev.gwarps, dev.agg,
               !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps, dev.d_hot, dev.n_hot, dev.sleep_ns,
-              dev.csr_pair && !dev.agg, Dbg{dev.dbg_skip}};
+              dev.csr_pair && !dev.agg, zero_y && dev.m > 0 && dev.pdl, Dbg{dev.dbg_skip}};
     const int smem = smem_bytes(dev);
     const void *fn = select_kernel(dev.dtype, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};
@@ -831,7 +838,7 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the zeroing kernel
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (zero_y && dev.m > 0 && dev.pdl) ? 1 : 0;
+    cfg.numAttrs = dev.pdl && ((zero_y && dev.m > 0) || follows) ? 1 : 0;
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return cuda_fail(e, "spmv kernel launch", err);
   }
