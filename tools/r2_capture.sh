@@ -28,3 +28,8 @@ done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cb_spmv_kernel -s 12 -c 1 -f -o gpurun_out/prof_uniform python tools/prof_kernel.py --config uniform --launches 3 > gpurun_out/ncu_uniform.log 2>&1; echo prof_uniform_rc=$?
 bash tools/ncu_metrics.sh > gpurun_out/ncu_metrics.log 2>&1; echo metrics_rc=$?
 bash tools/ncu_uniform_traffic.sh
+# the bounds-checking debug build over the GPU suite (compute-sanitizer is closed on the pool)
+if [ -f ab/check/libcbspmv.so ]; then
+  CBSPMV_LIB=$PWD/ab/check/libcbspmv.so timeout 1200 python -m pytest tests -m gpu -q -x --deselect tests/test_gpu_fullsize.py > gpurun_out/check_pytest.log 2>&1; echo check_pytest_rc=$?
+  CBSPMV_LIB=$PWD/ab/check/libcbspmv.so timeout 600 python tools/sanitize_run.py > gpurun_out/check_sanitize_run.txt 2>&1; echo check_run_rc=$?
+fi
