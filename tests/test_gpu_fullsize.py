@@ -11,8 +11,9 @@ power-iteration exchange).
     iteration sits at lambda = 50.  At n = 2^24 every quantity is dyadic (||1|| = 2^12), so
     lambda = 50 bitwise at all 100 steps.
 * format byte identity against the oracle's build at full size: the
-  clustered matrix (configs[3]) whole, and configs[4] as the 8-GPU run builds it — one row shard
-  of 2^22 rows with the global th0 decision (aggregation on).
+  clustered matrix (configs[3]) and the R-MAT graph (configs[2]) whole, and configs[4] as the
+  8-GPU run builds it — one row shard of 2^22 rows with the global th0 decision (aggregation on).
+  (configs[1], the Laplacian, is checked at full size by the CPU suite.)
 """
 import numpy as np
 import pytest
@@ -137,6 +138,13 @@ def test_clustered_full_format_equals_oracle():
     oracle's byte for byte."""
     _ok()
     _format_equal(synth.make("clustered"))
+
+
+def test_rmat_full_format_equals_oracle():
+    """configs[2] at full size (8 M rows, 131 M nnz, aggregation on by the th0 rule): the host
+    build's canonical format is the oracle's byte for byte."""
+    _ok()
+    _format_equal(synth.make("rmat"))
 
 
 def test_uniform_rank_shard_format_equals_oracle():
