@@ -158,7 +158,13 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
   const cb::Canon &c = P->canon;
   cb::Stream S;
   CbShape shape;
-  int st = cb_plan_stages(o.device, c.agg, &shape, err);
+  // aggregated matrices with >= 10 % CSR / DENSE blocks (the Laplacian's diagonal blocks): x warps
+  // gather those tiles through their restore entries ahead of the consumers (CBSPMV_XAGG=0/1
+  // overrides, read per build)
+  const int64_t n_cd = c.fmt_count[CBSPMV_FMT_CSR] + c.fmt_count[CBSPMV_FMT_DENSE];
+  bool agg_tiles = c.agg && c.nb > 0 && n_cd * 10 >= c.nb;
+  if (const char *v = std::getenv("CBSPMV_XAGG")) agg_tiles = c.agg && std::atoi(v) != 0;
+  int st = cb_plan_stages(o.device, c.agg, agg_tiles, &shape, err);
   if (st != CBSPMV_OK) return st;
   cb::StreamPlan plan;
   const bool on_device = P->dc != nullptr;  // records on the device: fill the stream there
@@ -180,7 +186,7 @@ static int upload_part(const cbspmv_options_t &o, int dtype, cudaStream_t cs, Pa
     if (st != CBSPMV_OK) return st;
   }
   st = cb::build_stream(c, shape.page_cap, vec_bytes(dtype), o.host_threads, &S, on_device ? &plan : nullptr, err,
-                        so, on_device ? &coords : nullptr);
+                        so, on_device ? &coords : nullptr, shape.xagg != 0);
   if (st != CBSPMV_OK) { cb::free_stream(&S); return st; }
   const int64_t npages = (int64_t)S.page_off.size() - 1;
   CbDevice &D = P->dev;

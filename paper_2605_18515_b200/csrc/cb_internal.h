@@ -167,8 +167,10 @@ struct SliceOpts {
 // x_size: bytes of one x element (sizes the x area that follows each page in its stage).
 // plan == nullptr: the whole stream is written to host memory (s->bytes); otherwise only the plan.
 // coords: the COO coordinate bytes when c.mtx does not hold the records (nullptr: c.mtx).
+// xagg: aggregated CSR / DENSE items also get an x-tile slot after the page (filled by the x warps).
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err, const SliceOpts &so = SliceOpts(), const CooCoords *coords = nullptr);
+                 std::string *err, const SliceOpts &so = SliceOpts(), const CooCoords *coords = nullptr,
+                 bool xagg = false);
 
 // Device-resident canonical arrays kept by the device builder for fill_stream_device.
 struct DevCanon {
@@ -239,6 +241,7 @@ int resolve_threads(int t);
 struct CbShape {
   int nstage = 12, groups = 4, gwarps = 7, xwarps = 3, page_cap = 19008;
   int hot_cap = 0;  // shared memory left for the hot x cache (bytes)
+  int xagg = 0;     // aggregated matrix whose CSR / DENSE tiles the x warps gather (restore entries)
 };
 
 struct CbDevice : CbShape {
@@ -271,7 +274,9 @@ struct CbDevice : CbShape {
 
 // Stage shape for a device (env CBSPMV_STAGES / CBSPMV_GROUPS / CBSPMV_GROUP_WARPS /
 // CBSPMV_PAGE_BYTES override the measured defaults; read per build).
-int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err);
+// agg_tiles: an aggregated matrix with many CSR / DENSE blocks (their x tiles are then gathered
+// by x warps into the stage, as for non-aggregated matrices).
+int cb_plan_stages(int device, int agg, bool agg_tiles, CbShape *sh, std::string *err);
 // Grid and page assignment for this device and stream (dev's shape already planned).
 int cb_configure(CbDevice *dev, std::string *err);
 // y (+)= A·(s·x); zero_y: clear y first; sumsq: nullptr or device double (s = 1/sqrt(*sumsq));

@@ -387,6 +387,7 @@ struct KParams {
   uint32_t sleep_ns;    // consumer / x-warp back-off between mbarrier probes (0: none)
   int csr_pair;         // non-aggregated: a warp takes two CSR blocks at once (one lane per row)
   int pdl_wait;         // launched dependent on the y-zeroing kernel: wait for it before any RED
+  int xagg;             // aggregated matrix whose CSR / DENSE tiles the x warps gather
   Dbg dbg;
 };
 
@@ -398,12 +399,19 @@ struct KParams {
 // matrix — while plain loads are limited only by the L1 / L2 request rate.)  A ragged last
 // block column or an x that is not 16-byte aligned is loaded per element with zero fill.
 template <typename V>
-__device__ __forceinline__ uint4 load_piece(const V *__restrict__ x, const uint4 &d, int q, bool vec, uint64_t pol) {
+__device__ __forceinline__ uint4 load_piece(const uint8_t *page, const V *__restrict__ x, const uint4 &d, int q,
+                                            bool vec, bool agg, uint64_t pol) {
   constexpr int kPer = 16 / (int)sizeof(V);
   const int nc = (d.w >> 2) & 31;
   const V *src = x + d.y + q;
   uint4 v;
-  if (vec && nc == 16) {
+  if (agg) {  // aggregated block: x[restore_cols[cols_offset[br] + bc*16 + c]], entries in the page
+    const uint32_t *res = reinterpret_cast<const uint32_t *>(page + d.y) + q;
+    V e[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; j++) e[j] = q + j < nc ? ldg_x(x + res[j], pol) : V(0);
+    memcpy(&v, e, 16);
+  } else if (vec && nc == 16) {
     asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(src), "l"(pol));
@@ -436,7 +444,7 @@ __device__ __forceinline__ void tile_page(const uint8_t *page, const V *__restri
       dst[r] = 0;
       if (it < ncd) {
         const uint4 d = descs[it];
-        v[r] = load_piece<V>(x, d, q, P.xvec != 0, pol);
+        v[r] = load_piece<V>(page, x, d, q, P.xvec != 0, P.agg != 0, pol);
         dst[r] = (d.w >> 16) + (uint32_t)q * (uint32_t)sizeof(V);
       }
     }
@@ -546,7 +554,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     // ---------------- x warps (non-aggregated matrices): x warp k fills the x tiles of pages
     // k, k + X, ... as they land, then arrives on the page's xready.  Dynamic claiming: X <= G,
     // so each x warp meets one of the G end markers (the last pages) and stops there.
-    if (P.agg) return;
+    if (P.agg && !P.xagg) return;
     const uint64_t pol = policy_evict_last();
     const int X = P.xwarps, k = warp - 1;
     int s = k;
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const uint8_t *page = ring + (size_t)s * P.stage;
     const uint32_t nitems = reinterpret_cast<const uint32_t *>(page)[0];
     if (dyn && nitems == cb::kEndItems) break;  // this group's end marker (nothing to release)
-    if (!P.agg) mbar_wait_sleep(&xrdy[s], parity, P.sleep_ns);
+    if (!P.agg || P.xagg) mbar_wait_sleep(&xrdy[s], parity, P.sleep_ns);
     const uint4 *descs = reinterpret_cast<const uint4 *>(page + cb::kPageHeader);
     const int n = (dbg.skip() & 4) ? 0 : (int)nitems;
     const int ncd = (int)reinterpret_cast<const uint32_t *>(page)[1];
@@ -610,7 +618,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
           const uint4 e = descs[k + W];
           CB_CHECK((d.z >> 16) + (uint32_t)sizeof(M) * (((d.w >> 8) & 0xFF) + 1) <= (uint32_t)P.stage &&
                    (e.z >> 16) + (uint32_t)sizeof(M) * (((e.w >> 8) & 0xFF) + 1) <= (uint32_t)P.stage);
-          CB_CHECK((int64_t)d.x < P.m && (int64_t)e.x < P.m && (int64_t)d.y < P.n && (int64_t)e.y < P.n &&
+          // (d.y: the tile's first column, or with aggregation the page offset of its restore entries)
+          CB_CHECK((int64_t)d.x < P.m && (int64_t)e.x < P.m &&
+                   (P.agg ? d.y + 64 <= (uint32_t)P.stage && e.y + 64 <= (uint32_t)P.stage
+                          : (int64_t)d.y < P.n && (int64_t)e.y < P.n) &&
                    (d.w >> 16) + 16 * sizeof(V) <= (uint32_t)P.stage && (e.w >> 16) + 16 * sizeof(V) <= (uint32_t)P.stage);
         }
         csr_pair<M, V, SCALED>(page, d, descs[k + W], scale, y, lane, dbg);
@@ -623,11 +634,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
                                                           : (d.z >> 16) + (uint32_t)sizeof(M) * 256;
         CB_CHECK(((d.w & 3) == CBSPMV_FMT_CSR || (d.w & 3) == CBSPMV_FMT_DENSE) && nc <= 16 && rec <= (uint32_t)P.stage &&
                  (int64_t)d.x < P.m);
-        CB_CHECK(P.agg ? d.y + 4 * nc <= (uint32_t)P.stage : ((int64_t)d.y < P.n && (d.w >> 16) + 16 * sizeof(V) <= (uint32_t)P.stage));
+        CB_CHECK(P.agg ? d.y + 4 * nc <= (uint32_t)P.stage : (int64_t)d.y < P.n);
+        CB_CHECK((P.agg && !P.xagg) || (d.w >> 16) + 16 * sizeof(V) <= (uint32_t)P.stage);
         if (P.agg && lane < (int)nc) CB_CHECK((int64_t)reinterpret_cast<const uint32_t *>(page + d.y)[lane] < P.n);
       }
-      const V *xt = P.agg ? agg_tile<V>(page, d, x, wscratch, lane, xpol)
-                          : reinterpret_cast<const V *>(page + (d.w >> 16));
+      const V *xt = P.agg && !P.xagg ? agg_tile<V>(page, d, x, wscratch, lane, xpol)
+                                     : reinterpret_cast<const V *>(page + (d.w >> 16));
       if ((d.w & 3) == CBSPMV_FMT_CSR) csr_path<M, V, SCALED>(page, d, xt, scale, y, lane, dbg);
       else dense_path<M, V, SCALED>(page, d, xt, scale, y, P.m, lane, dbg);
     }
@@ -717,7 +729,7 @@ int env_int(const char *k, int d) {
 // Launch shape, read once per built handle (so a test can build handles with different shapes
 // in one process): S stages, G consumer groups of W warps (G divides S), and the stage bytes
 // that fill the opt-in shared memory.  Defaults measured on B200.
-int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err) {
+int cb_plan_stages(int device, int agg, bool agg_tiles, CbShape *sh, std::string *err) {
   int optin = 0;
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute", err);
@@ -730,9 +742,12 @@ int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err) {
   // 20 KB: ~120 KB shared, ~100 KB L1; 12 x 19 KB: 1.10 / 13.1, 4 x 24 KB: 0.72, 2 x 32 KB: 1.00).
   // Non-aggregated matrices stream their x tiles with plain loads and need the deep ring
   // (clustered: 12 x 19 KB 0.72-0.75 ms, 8 x 19 KB 0.82, 8 x 22 KB 0.78).
+  // Aggregated matrices with many CSR / DENSE blocks (agg_tiles, the Laplacian) keep the aggregated
+  // shape but trade one consumer warp per group for two x warps that gather those tiles.
+  const bool xagg = agg && agg_tiles;
   const int G = std::max(1, env_int("CBSPMV_GROUPS", agg ? 2 : 4));
-  const int W = std::max(1, env_int("CBSPMV_GROUP_WARPS", agg ? 15 : 7));
-  const int X = agg ? 0 : std::max(1, std::min(G, env_int("CBSPMV_XWARPS", 3)));  // X <= G (end markers)
+  const int W = std::max(1, env_int("CBSPMV_GROUP_WARPS", xagg ? 14 : agg ? 15 : 7));
+  const int X = agg && !xagg ? 0 : std::max(1, std::min(G, env_int("CBSPMV_XWARPS", xagg ? 2 : 3)));  // X <= G (end markers)
   int S = std::min(kMaxStages, std::max(G, env_int("CBSPMV_STAGES", agg ? 6 : 12)));
   S -= S % G;  // G | S: every stage belongs to one group
   if (1 + X + G * W > kMaxThreads / 32) {
@@ -756,6 +771,7 @@ int cb_plan_stages(int device, int agg, CbShape *sh, std::string *err) {
   sh->xwarps = X;
   sh->page_cap = cap;
   sh->hot_cap = std::max(0, optin - kSmemHeader - S * cap - scratch_bytes(probe));
+  sh->xagg = xagg ? 1 : 0;
   return CBSPMV_OK;
 }
 
@@ -824,7 +840,8 @@ int cb_launch_spmv(const CbDevice &dev, const void *x, void *y, const double *su
     KParams P{dev.d_stream, dev.d_page_off, dev.d_cta_page, ctr, (uint32_t)dev.n_pages, dev.claim_chunk,
               ctr ? 0 : dev.strided, dev.m, dev.n, sumsq, dev.page_cap, dev.nstage, dev.groups, dev.gwarps, dev.agg,
               !dev.agg && ((uintptr_t)x % 16 == 0), dev.xwarps, dev.d_hot, dev.n_hot, dev.sleep_ns,
-              dev.csr_pair && !dev.agg, zero_y && dev.m > 0 && dev.pdl, Dbg{dev.dbg_skip}};
+              dev.csr_pair && (!dev.agg || dev.xagg), zero_y && dev.m > 0 && dev.pdl, dev.xagg,
+              Dbg{dev.dbg_skip}};
     const int smem = smem_bytes(dev);
     const void *fn = select_kernel(dev.dtype, sumsq != nullptr);
     void *args[] = {&P, const_cast<void **>(&x), &y};

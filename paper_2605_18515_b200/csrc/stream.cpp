@@ -126,13 +126,14 @@ void free_stream(Stream *s) {
 }
 
 int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *s, StreamPlan *plan,
-                 std::string *err, const SliceOpts &so, const CooCoords *coords) {
+                 std::string *err, const SliceOpts &so, const CooCoords *coords, bool xagg) {
   if (c.blk != 16) { *err = "the device page stream needs 16x16 blocks"; return CBSPMV_EUNSUPPORTED; }
   if (page_cap > kMaxPageCap || page_cap < 1024) { *err = "stage capacity out of range"; return CBSPMV_EUNSUPPORTED; }
   if (so.run_max < 1 || so.run_max > kMaxRun) { *err = "run_max out of range [1, 255]"; return CBSPMV_EINVAL; }
   const int T = resolve_threads(threads);
   const int S = c.val_size;
   const Shape sh{S, x_size, so.run_max};
+  const bool xtiles = !c.agg || xagg;  // CSR / DENSE items get an x-tile slot after the page
   PhaseTimer tm;
   auto coord = [&](int64_t i) -> const uint8_t * {
     return coords ? coords->bytes.data() + coords->off[i] : c.mtx.data() + c.vp[i];
@@ -243,7 +244,7 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
           }
           nx.E += c.nnzb[i];
         } else {
-          nx.items++; nx.rec += rec[i]; nx.xb += c.agg ? 0 : 16 * (int64_t)x_size;
+          nx.items++; nx.rec += rec[i]; nx.xb += xtiles ? 16 * (int64_t)x_size : 0;
         }
         nx.blocks++;
         if (sh.stage_bytes(nx) <= page_cap) {
@@ -421,10 +422,10 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
         d[1] = c.agg ? (uint32_t)res : (uint32_t)c.bc[i] * (uint32_t)c.blk;
         d[2] = (uint32_t)body | ((uint32_t)vals << 16);
         d[3] = (uint32_t)type | ((uint32_t)ncol[i] << 2) | ((uint32_t)(k - 1) << 8) |
-               (c.agg ? 0u : (uint32_t)xpos << 16);
+               (xtiles ? (uint32_t)xpos << 16 : 0u);
         std::memcpy(page + desc0 + kDescBytes * it, d, 16);
         it++;
-        if (!c.agg) xpos += 16 * (int64_t)x_size;
+        if (xtiles) xpos += 16 * (int64_t)x_size;
         if (plan) {
           plan->rec_dst[i] = off[p] + (uint64_t)body;
           if (c.agg) plan->res_dst[i] = off[p] + (uint64_t)res;

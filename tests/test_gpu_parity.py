@@ -266,7 +266,7 @@ def _long_run_matrix():
 @pytest.mark.parametrize("dtype", ["f64", "f32f64"])
 @pytest.mark.parametrize("device_build", [0, 1])
 @pytest.mark.parametrize("runopt", ["", "RUN_MAX=7", "RUN_MAX=32", "RUN_ORDER=row", "HOT_MIN_PCT=0",
-                                    "HOT_MIN_PCT=0,HOT_BYTES=256"])
+                                    "HOT_MIN_PCT=0,HOT_BYTES=256", "XAGG=1", "XAGG=0"])
 def test_device_stream_encodes_canonical_format(name, dtype, device_build, runopt, monkeypatch):
     """What is on the device is exactly the canonical format (slot order): pages tile the slot
     order; CSR / DENSE records byte-equal (DENSE re-laid lane-major), their restore entries equal
@@ -308,6 +308,9 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build, runop
     vdt = np.float64 if S == 8 else np.float32
     xs = 8  # x / y element bytes (f64 and f32f64)
     agg = h.info["agg"]
+    n_cd = int(np.sum(ex["type_per_blk"] != 0))
+    xagg = bool(agg) and (runopt == "XAGG=1" or (runopt != "XAGG=0" and n_cd * 10 >= ex["nb"]))
+    xtiles = not agg or xagg
     mtx, vp = ex["mtx_data"], ex["vp_per_blk"].astype(np.int64)
     nxt = 0
     shapes = []
@@ -322,10 +325,11 @@ def test_device_stream_encodes_canonical_format(name, dtype, device_build, runop
         slices = [it for it in P["items"] if it["type"] == 0]
         assert [it["type"] for it in P["items"]] == [1 if ex["type_per_blk"][i] == 1 else 2 for i in cd] + [0] * len(slices)
         assert P["ncd"] == len(cd)
-        # x tiles (non-aggregated CSR / DENSE only): 16 values each, consecutive after the page
+        # x tiles (CSR / DENSE items of non-aggregated matrices, and of aggregated ones with
+        # >= 10 % CSR / DENSE blocks or CBSPMV_XAGG=1): 16 values each, consecutive after the page
         end = len(pg)
         for it in P["items"]:
-            if it["type"] and not agg:
+            if it["type"] and xtiles:
                 assert it["xslot"] == end
                 end += 16 * xs
             elif it["type"]:
@@ -656,7 +660,8 @@ def test_spmv_host_batch_pipelined(count, dtype):
 _RUNOPTS = [{"CBSPMV_COO_RUNS": "0"}, {"CBSPMV_RUN_MAX": "1"}, {"CBSPMV_RUN_MAX": "2"}, {"CBSPMV_RUN_MAX": "5"},
             {}, {"CBSPMV_RUN_MAX": "32"}, {"CBSPMV_RUN_MAX": "255"}, {"CBSPMV_RUN_ORDER": "row"},
             {"CBSPMV_RUN_ORDER": "row", "CBSPMV_RUN_MAX": "3"}, {"CBSPMV_HOT_MIN_PCT": "0"},
-            {"CBSPMV_HOT_MIN_PCT": "0", "CBSPMV_HOT_BYTES": "256"}, {"CBSPMV_HOT_BYTES": "0"}]
+            {"CBSPMV_HOT_MIN_PCT": "0", "CBSPMV_HOT_BYTES": "256"}, {"CBSPMV_HOT_BYTES": "0"},
+            {"CBSPMV_XAGG": "1"}, {"CBSPMV_XAGG": "1", "CBSPMV_CSR_PAIR": "0"}]
 _runid = lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()) or "default"
 
 
@@ -727,7 +732,8 @@ _SHAPES = [
     {"CBSPMV_STAGES": "30", "CBSPMV_GROUPS": "5", "CBSPMV_GROUP_WARPS": "5", "CBSPMV_XWARPS": "5"},
     {"CBSPMV_STAGES": "16", "CBSPMV_GROUPS": "4", "CBSPMV_GROUP_WARPS": "6", "CBSPMV_XWARPS": "4"},
     {"CBSPMV_PAGE_BYTES": "4096"}, {"CBSPMV_WAIT_SLEEP_NS": "128"}, {"CBSPMV_PDL": "0"},
-    {"CBSPMV_CSR_PAIR": "1"}, {"CBSPMV_CSR_PAIR": "0"},
+    {"CBSPMV_CSR_PAIR": "1"}, {"CBSPMV_CSR_PAIR": "0"}, {"CBSPMV_XAGG": "1"}, {"CBSPMV_XAGG": "0"},
+    {"CBSPMV_XAGG": "1", "CBSPMV_GROUPS": "2", "CBSPMV_GROUP_WARPS": "12", "CBSPMV_XWARPS": "1"},
 ]
 
 
