@@ -163,13 +163,17 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
   };
   std::vector<uint32_t> hot_slot;  // column -> slot (kNotHot: not cached); empty: no cache
   constexpr uint32_t kNotHot = 0xFFFFFFFFu;
+  // every persistent CTA copies the H hot values per launch: the cache must save more gathers than
+  // kHotCostFactor x (CTAs x H); CTAs = the B200's 148 SMs (the launch grid; a cost estimate only)
+  constexpr int64_t kHotCopyCtas = 148, kHotCostFactor = 4;
   s->hot_cols.clear();
   {
     const int64_t H = so.hot_bytes > 0 ? so.hot_bytes / x_size : 0;
     int64_t n_coo = 0;
     for (int64_t i = 0; i < c.nb; i++) n_coo += c.type[i] == CBSPMV_FMT_COO ? c.nnzb[i] : 0;
     const bool force = so.hot_min_pct == 0;
-    if (H > 0 && n_coo > 0 && c.n <= (int64_t)1 << 27 && (force || n_coo >= 4 * 148 * H)) {  // count array <= 512 MB
+    if (H > 0 && n_coo > 0 && c.n <= (int64_t)1 << 27 &&  // count array <= 512 MB
+        (force || n_coo >= kHotCostFactor * kHotCopyCtas * H)) {
       // estimate on every 251st COO block first (uniform-like matrices stop here)
       std::vector<uint32_t> samp;
       for (int64_t i = 0; i < c.nb; i += 251)
@@ -209,7 +213,8 @@ int build_stream(const Canon &c, int page_cap, int x_size, int threads, Stream *
         }
         int64_t covered = 0;
         for (uint32_t j : cand) covered += hist[j].load(std::memory_order_relaxed);
-        if (force || (covered * 100 >= (int64_t)so.hot_min_pct * n_coo && covered >= 4 * 148 * (int64_t)cand.size())) {
+        if (force || (covered * 100 >= (int64_t)so.hot_min_pct * n_coo &&
+                      covered >= kHotCostFactor * kHotCopyCtas * (int64_t)cand.size())) {
           std::sort(cand.begin(), cand.end());
           hot_slot.assign((size_t)c.n, kNotHot);
           for (size_t k = 0; k < cand.size(); k++) hot_slot[cand[k]] = (uint32_t)k;
